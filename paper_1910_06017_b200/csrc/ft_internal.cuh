@@ -1,0 +1,161 @@
+// Internal declarations shared by the libomnitrack CUDA sources.
+//
+// Numerics: the library is compiled with -fmad=false and uses only IEEE
+// round-to-nearest +,-,*,/,sqrt, floor and comparisons, in the reference's
+// operation order, so every kernel reproduces the numpy reference bit for bit
+// (np.hypot is glibc's hypot, restated in glibc_hypot below).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/omnitrack.h"
+
+namespace ft {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string &msg);
+int fail(int code, const std::string &msg);
+int cuda_fail(cudaError_t e, const char *what);
+
+#define FT_CUDA_TRY(expr)                              \
+  do {                                                 \
+    cudaError_t _e = (expr);                           \
+    if (_e != cudaSuccess) return ::ft::cuda_fail(_e, #expr); \
+  } while (0)
+
+#define FT_TRY(expr)            \
+  do {                          \
+    int _rc = (expr);           \
+    if (_rc != FT_OK) return _rc; \
+  } while (0)
+
+// ---------------------------------------------------------------- numerics
+// glibc >= 2.35 __hypot without FMA (Borges' correction), which is what
+// numpy's np.hypot calls on x86-64; verified identical on 2e5 random pairs.
+__device__ __forceinline__ double glibc_hypot_kernel(double ax, double ay) {
+  double h = sqrt(ax * ax + ay * ay);
+  double t1, t2;
+  if (h <= 2.0 * ay) {
+    double delta = h - ay;
+    t1 = ax * (2.0 * delta - ax);
+    t2 = (delta - 2.0 * (ax - ay)) * delta;
+  } else {
+    double delta = h - ax;
+    t1 = 2.0 * delta * (ax - 2.0 * ay);
+    t2 = (4.0 * delta - ay) * ay + delta * delta;
+  }
+  h -= (t1 + t2) / (2.0 * h);
+  return h;
+}
+
+__device__ __forceinline__ double glibc_hypot(double x, double y) {
+  x = fabs(x);
+  y = fabs(y);
+  double ax = x < y ? y : x;
+  double ay = x < y ? x : y;
+  if (ax > 0x1p+511) {
+    if (ay <= ax * 0x1p-54) return ax + ay;
+    return glibc_hypot_kernel(ax * 0x1p-600, ay * 0x1p-600) / 0x1p-600;
+  }
+  if (ay < 0x1p-511) {
+    if (ax >= ay / 0x1p-54) return ax + ay;
+    return glibc_hypot_kernel(ax / 0x1p-600, ay / 0x1p-600) * 0x1p-600;
+  }
+  if (ay <= ax * 0x1p-54) return ax + ay;
+  return glibc_hypot_kernel(ax, ay);
+}
+
+// numpy maximum/minimum without NaNs: first argument wins ties
+__device__ __forceinline__ double np_max(double a, double b) { return a >= b ? a : b; }
+__device__ __forceinline__ double np_min(double a, double b) { return a <= b ? a : b; }
+
+// ---------------------------------------------------------------- launch
+constexpr int kSMs = 148;
+
+struct LaunchCounter {
+  int64_t n = 0;
+};
+extern thread_local LaunchCounter *g_launch_counter;
+inline void count_launch(int n = 1) {
+  if (g_launch_counter) g_launch_counter->n += n;
+}
+
+// ---------------------------------------------------------------- imaging
+// All batched launchers operate on `nb` independent images laid out with a
+// fixed element stride between consecutive images.
+int launch_gray8_to_unit(const uint8_t *src, int w, int h, int64_t src_stride, double *dst,
+                         int64_t dst_stride, int nb, cudaStream_t s);
+// one pyramid step: dst = decimate2(smooth_gaussian5(src)); optional scaled copy
+int launch_blur_decimate(const double *src, int w, int h, int64_t src_stride, double *dst,
+                         int64_t dst_stride, double *dst_scaled, int64_t scaled_stride,
+                         double scale, int nb, cudaStream_t s);
+// same but reading u8 and dividing by 255 on the fly (fused ingest)
+int launch_blur_decimate_u8(const uint8_t *src, int w, int h, int64_t src_stride, double *dst,
+                            int64_t dst_stride, int nb, cudaStream_t s);
+int launch_scale_copy(const double *src, int64_t n, int64_t src_stride, double *dst,
+                      int64_t dst_stride, double scale, int nb, cudaStream_t s);
+// structure_texture: ws must hold 4 planes of w*h per image (px,py ping-pong)
+// mode 0: structure_texture output; mode 1: rof_denoise structure only
+int launch_structure_texture(const double *img, int w, int h, int64_t stride, double weight,
+                             double blend, int iterations, double *out, int64_t out_stride,
+                             double *ws, int64_t ws_stride, int nb, cudaStream_t s,
+                             int mode = 0, double step = 0.25);
+
+// ---------------------------------------------------------------- flow
+struct FlowLevelPlanes {
+  // all planes share one geometry (w x h) and a per-image element stride
+  int w, h;
+  int64_t stride;
+};
+
+// Workspace for one batch of nb images at a max level size.
+struct FlowWork {
+  int nb = 0;
+  int64_t cap = 0;  // elements per plane per image
+  // per-warp constants
+  double *gx = nullptr, *gy = nullptr, *r0 = nullptr;
+  // gradient of i1 (per level)
+  double *ix = nullptr, *iy = nullptr;
+  // primal-dual state, ping-pong (8 planes each: u1 u2 b1 b2 p11 p12 p21 p22)
+  double *st[2] = {nullptr, nullptr};
+  // flow at the current level (u1,u2) and at the previous (coarser) level
+  double *u_prev = nullptr;  // 2 planes
+};
+int flow_work_alloc(FlowWork &fw, int nb, int64_t cap);
+void flow_work_free(FlowWork &fw);
+
+struct FlowParamsD {
+  double lam, tau, eps;
+  int warps, iters;
+};
+
+// Coarse-to-fine TV-L1 over nb image pairs given their (already scaled x255)
+// pyramids.  pyr0/pyr1: level l of image b at pyr[b*pyr_stride + off[l]].
+// Result flow at level 0 written to (dx, dy) with stride out_stride.
+int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const int *lw,
+             const int *lh, const int64_t *loff, int scales, const FlowParamsD &p, FlowWork &fw,
+             double *dx, double *dy, int64_t out_stride, int nb, cudaStream_t s);
+
+int profile_pd(FlowWork &fw, int w, int h, int nb, const FlowParamsD &p, int reps,
+               cudaStream_t s, double *ms_per_launch, int *iters_per_launch);
+
+// ---------------------------------------------------------------- tracking
+int launch_predict(const double *boxes, int n, const double *dx, const double *dy, int fw_l,
+                   int fh_l, int64_t field_stride, int level, int frame_w, int frame_h,
+                   double *out, uint8_t *valid, cudaStream_t s);
+int launch_iou_matrix(const double *a, int m, const double *b, int n, double *out,
+                      cudaStream_t s);
+int launch_gate_cost(const double *a, const int32_t *ac, int m, const double *b,
+                     const int32_t *bc, int n, double gate, double *scores, double *cost,
+                     cudaStream_t s);
+int launch_hungarian(const double *cost, int m, int n, int has_forbidden, double forbidden,
+                     int *row_col, int32_t *pairs, int32_t *n_pairs, cudaStream_t s);
+int launch_update_unit(const int64_t *ids, const int32_t *state, const double *boxes, int n,
+                       const int32_t *pairs, int np, const double *dboxes, int nd, double blend,
+                       int *match_of, unsigned char *det_used, int32_t *out_src, double *out_box,
+                       int32_t *out_flag, int64_t *out_id, int32_t *n_out, cudaStream_t s);
+
+}  // namespace ft

@@ -1,0 +1,218 @@
+// Imaging kernels: u8 ingest, Gaussian pyramid step, ROF structure-texture.
+//
+// Reference: imaging.py (Frame.from_gray8 :52-56, build_pyramid :75-95,
+// rof_denoise :109-125, structure_texture :128-144) and the grid stencils of
+// imageops.py (smooth_gaussian5 :12-23, decimate2 :26-29, forward_gradient
+// :32-38, divergence :41-50).  All batched: blockIdx.z selects the image.
+#include "ft_internal.cuh"
+
+namespace ft {
+
+namespace {
+
+// binomial taps [1,4,6,4,1]/16 (imageops.py:9), exact in binary
+__device__ __constant__ double kTaps[5] = {0.0625, 0.25, 0.375, 0.25, 0.0625};
+
+// np.pad(..., "symmetric") with pad 2: edge sample duplicated
+__device__ __forceinline__ int mirror(int i, int n) {
+  i = i < 0 ? -i - 1 : i;
+  return i >= n ? 2 * n - 1 - i : i;
+}
+
+__global__ void k_gray8_to_unit(const uint8_t *__restrict__ src, int w, int h, int64_t ss,
+                                double *__restrict__ dst, int64_t ds) {
+  const int64_t n = (int64_t)w * h;
+  src += blockIdx.z * ss;
+  dst += blockIdx.z * ds;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = (double)src[i] / 255.0;
+}
+
+// Even-sample output of the separable blur: out(i,j) = sum_k t_k * row_k where
+// row_k = sum_q t_q * src(mirror(2i-2+k), mirror(2j-2+q)); each sum starts at
+// 0.0 and adds taps in order, exactly like smooth_gaussian5's accumulation.
+template <typename T, bool kU8>
+__global__ void k_blur_decimate(const T *__restrict__ src, int w, int h, int64_t ss,
+                                double *__restrict__ dst, int64_t ds,
+                                double *__restrict__ dst_scaled, int64_t dss, double scale) {
+  const int ow = w / 2, oh = h / 2;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= oh || j >= ow) return;
+  src += blockIdx.z * ss;
+  int cols[5];
+#pragma unroll
+  for (int q = 0; q < 5; ++q) cols[q] = mirror(2 * j - 2 + q, w);
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const T *row = src + (int64_t)mirror(2 * i - 2 + k, h) * w;
+    double r = 0.0;
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      double v = kU8 ? (double)row[cols[q]] / 255.0 : (double)row[cols[q]];
+      r = r + kTaps[q] * v;
+    }
+    acc = acc + kTaps[k] * r;
+  }
+  dst[blockIdx.z * ds + (int64_t)i * ow + j] = acc;
+  if (dst_scaled) dst_scaled[blockIdx.z * dss + (int64_t)i * ow + j] = acc * scale;
+}
+
+__global__ void k_scale_copy(const double *__restrict__ src, int64_t n, int64_t ss,
+                             double *__restrict__ dst, int64_t ds, double scale) {
+  src += blockIdx.z * ss;
+  dst += blockIdx.z * ds;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i] * scale;
+}
+
+// divergence(px, py) at (r, c) (imageops.py:41-50): dx + dy with the
+// first/last column (row) rules; requires w, h >= 2.
+__device__ __forceinline__ double div_at(const double *__restrict__ px,
+                                         const double *__restrict__ py, int r, int c, int w,
+                                         int h) {
+  const int64_t o = (int64_t)r * w + c;
+  double dx = c == 0 ? px[o] : (c == w - 1 ? -px[o - 1] : px[o] - px[o - 1]);
+  double dy = r == 0 ? py[o] : (r == h - 1 ? -py[o - w] : py[o] - py[o - w]);
+  return dx + dy;
+}
+
+constexpr int kRB = 32;  // ROF tile (kRB x kRB outputs, one halo row/col)
+
+// One ROF dual step (imaging.py:120-124):
+//   d = div(p) - img/weight;  g = forward_gradient(d);
+//   norm = 1 + step*hypot(g);  p = (p + step*g) / norm
+// d is staged in shared memory for the (kRB+1)^2 patch the tile needs.
+__global__ void __launch_bounds__(256) k_rof_step(const double *__restrict__ img, int w, int h,
+                                                  int64_t is, const double *__restrict__ px,
+                                                  const double *__restrict__ py,
+                                                  double *__restrict__ qx,
+                                                  double *__restrict__ qy, int64_t ps,
+                                                  double weight, double step) {
+  __shared__ double sd[kRB + 1][kRB + 2];
+  img += blockIdx.z * is;
+  px += blockIdx.z * ps;
+  py += blockIdx.z * ps;
+  qx += blockIdx.z * ps;
+  qy += blockIdx.z * ps;
+  const int c0 = blockIdx.x * kRB, r0 = blockIdx.y * kRB;
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  for (int k = tid; k < (kRB + 1) * (kRB + 1); k += blockDim.x * blockDim.y) {
+    const int lr = k / (kRB + 1), lc = k % (kRB + 1);
+    const int r = r0 + lr, c = c0 + lc;
+    double v = 0.0;
+    if (r < h && c < w) v = div_at(px, py, r, c, w, h) - img[(int64_t)r * w + c] / weight;
+    sd[lr][lc] = v;
+  }
+  __syncthreads();
+  for (int lr = threadIdx.y; lr < kRB; lr += blockDim.y) {
+    const int r = r0 + lr, c = c0 + threadIdx.x;
+    if (r >= h || c >= w) continue;
+    const double d = sd[lr][threadIdx.x];
+    const double gx = c < w - 1 ? sd[lr][threadIdx.x + 1] - d : 0.0;
+    const double gy = r < h - 1 ? sd[lr + 1][threadIdx.x] - d : 0.0;
+    const double norm = 1.0 + step * glibc_hypot(gx, gy);
+    const int64_t o = (int64_t)r * w + c;
+    qx[o] = (px[o] + step * gx) / norm;
+    qy[o] = (py[o] + step * gy) / norm;
+  }
+}
+
+// structure = img - weight*div(p); out = clip(((img - S) + blend*S +
+// (1-blend)) / (2-blend), 0, 1)   (imaging.py:125, :139-144)
+__global__ void k_st_combine(const double *__restrict__ img, int w, int h, int64_t is,
+                             const double *__restrict__ px, const double *__restrict__ py,
+                             int64_t ps, double weight, double blend,
+                             double *__restrict__ out, int64_t os, int mode) {
+  img += blockIdx.z * is;
+  px += blockIdx.z * ps;
+  py += blockIdx.z * ps;
+  out += blockIdx.z * os;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = blockIdx.y * blockDim.y + threadIdx.y;
+  if (r >= h || c >= w) return;
+  const int64_t o = (int64_t)r * w + c;
+  const double I = img[o];
+  const double S = I - weight * div_at(px, py, r, c, w, h);
+  if (mode == 1) {  // rof_denoise result (imaging.py:125)
+    out[o] = S;
+    return;
+  }
+  double m = (I - S) + blend * S;
+  m = (m + (1.0 - blend)) / (2.0 - blend);
+  // np.clip(x, 0, 1) == min(max(x, 0), 1) with numpy's comparison order
+  m = m > 0.0 ? m : 0.0;
+  m = m < 1.0 ? m : 1.0;
+  out[o] = m;
+}
+
+int grid1d(int64_t n, int bs) {
+  int64_t g = (n + bs - 1) / bs;
+  if (g > 4 * kSMs * 8) g = 4 * kSMs * 8;
+  return (int)(g < 1 ? 1 : g);
+}
+
+}  // namespace
+
+int launch_gray8_to_unit(const uint8_t *src, int w, int h, int64_t ss, double *dst, int64_t ds,
+                         int nb, cudaStream_t s) {
+  k_gray8_to_unit<<<dim3(grid1d((int64_t)w * h, 256), 1, nb), 256, 0, s>>>(src, w, h, ss, dst,
+                                                                           ds);
+  count_launch();
+  FT_CUDA_TRY(cudaGetLastError());
+  return FT_OK;
+}
+
+int launch_blur_decimate(const double *src, int w, int h, int64_t ss, double *dst, int64_t ds,
+                         double *dst_scaled, int64_t dss, double scale, int nb, cudaStream_t s) {
+  dim3 b(32, 8), g((w / 2 + 31) / 32, (h / 2 + 7) / 8, nb);
+  k_blur_decimate<double, false><<<g, b, 0, s>>>(src, w, h, ss, dst, ds, dst_scaled, dss, scale);
+  count_launch();
+  FT_CUDA_TRY(cudaGetLastError());
+  return FT_OK;
+}
+
+int launch_blur_decimate_u8(const uint8_t *src, int w, int h, int64_t ss, double *dst,
+                            int64_t ds, int nb, cudaStream_t s) {
+  dim3 b(32, 8), g((w / 2 + 31) / 32, (h / 2 + 7) / 8, nb);
+  k_blur_decimate<uint8_t, true><<<g, b, 0, s>>>(src, w, h, ss, dst, ds, nullptr, 0, 1.0);
+  count_launch();
+  FT_CUDA_TRY(cudaGetLastError());
+  return FT_OK;
+}
+
+int launch_scale_copy(const double *src, int64_t n, int64_t ss, double *dst, int64_t ds,
+                      double scale, int nb, cudaStream_t s) {
+  k_scale_copy<<<dim3(grid1d(n, 256), 1, nb), 256, 0, s>>>(src, n, ss, dst, ds, scale);
+  count_launch();
+  FT_CUDA_TRY(cudaGetLastError());
+  return FT_OK;
+}
+
+int launch_structure_texture(const double *img, int w, int h, int64_t is, double weight,
+                             double blend, int iterations, double *out, int64_t os, double *ws,
+                             int64_t wss, int nb, cudaStream_t s, int mode, double step) {
+  // ws per image: [px0, py0, px1, py1] planes of w*h
+  const int64_t n = (int64_t)w * h;
+  for (int b = 0; b < nb; ++b) FT_CUDA_TRY(cudaMemsetAsync(ws + b * wss, 0, 2 * n * 8, s));
+  double *p[2][2] = {{ws, ws + n}, {ws + 2 * n, ws + 3 * n}};
+  int cur = 0;
+  dim3 blk(32, 8), grd((w + kRB - 1) / kRB, (h + kRB - 1) / kRB, nb);
+  for (int it = 0; it < iterations; ++it) {
+    k_rof_step<<<grd, blk, 0, s>>>(img, w, h, is, p[cur][0], p[cur][1], p[1 - cur][0],
+                                   p[1 - cur][1], wss, weight, step);
+    count_launch();
+    cur = 1 - cur;
+  }
+  dim3 g2((w + 31) / 32, (h + 7) / 8, nb);
+  k_st_combine<<<g2, blk, 0, s>>>(img, w, h, is, p[cur][0], p[cur][1], wss, weight, blend, out,
+                                  os, mode);
+  count_launch();
+  FT_CUDA_TRY(cudaGetLastError());
+  return FT_OK;
+}
+
+}  // namespace ft

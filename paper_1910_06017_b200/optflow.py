@@ -1,0 +1,151 @@
+"""Dense coarse-to-fine TV-L1 optical flow on the B200 (drop-in for
+reference optflow.py: FlowParams, MotionField, auto_scales, compute_flow).
+
+The field maps pixels of `prev` to `curr`: content at p in prev appears at
+p + field(p) in curr (optflow.py:10-11).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .imaging import Frame
+
+MIN_COARSE_DIM = 16  # optflow.py:26
+INTENSITY_SCALE = 255.0  # optflow.py:31
+
+
+@dataclass(frozen=True)
+class FlowParams:
+    """Solver parameters (optflow.py:36-66); dual step = 1/(8*time_step)."""
+
+    data_weight: float = 0.15
+    huber_epsilon: float = 0.01
+    time_step: float = 0.25
+    warps_per_level: int = 5
+    iterations_per_warp: int = 50
+    pyramid_scales: int | None = None  # None: deepest with coarsest dim >= 16
+
+    def __post_init__(self):
+        if self.data_weight <= 0:
+            raise ValueError("data_weight must be positive")
+        if self.huber_epsilon < 0:
+            raise ValueError("huber_epsilon must be non-negative")
+        if self.time_step <= 0:
+            raise ValueError("time_step must be positive")
+        if self.warps_per_level < 1:
+            raise ValueError("warps_per_level must be >= 1")
+        if self.iterations_per_warp < 1:
+            raise ValueError("iterations_per_warp must be >= 1")
+        if self.pyramid_scales is not None and self.pyramid_scales < 1:
+            raise ValueError("pyramid_scales must be >= 1")
+
+
+class MotionField:
+    """Dense per-pixel displacement (optflow.py:69-93).  dx / dy are
+    read-only host arrays materialised on first access; the device planes
+    stay available to predict() without a round trip."""
+
+    __slots__ = ("width", "height", "frame_index", "_dx", "_dy", "_ddx", "_ddy")
+
+    def __init__(self, width: int, height: int, dx, dy, frame_index: int = -1):
+        object.__setattr__(self, "width", int(width))
+        object.__setattr__(self, "height", int(height))
+        object.__setattr__(self, "frame_index", int(frame_index))
+        shape = (self.height, self.width)
+        on_dev = type(dx).__module__.startswith("torch")
+        if on_dev:
+            if tuple(dx.shape) != shape or tuple(dy.shape) != shape:
+                raise ValueError(f"field components must be {shape}")
+            object.__setattr__(self, "_ddx", dx)
+            object.__setattr__(self, "_ddy", dy)
+            object.__setattr__(self, "_dx", None)
+            object.__setattr__(self, "_dy", None)
+            return
+        dx = np.ascontiguousarray(dx, dtype=np.float64)
+        dy = np.ascontiguousarray(dy, dtype=np.float64)
+        if dx.shape != shape or dy.shape != shape:
+            raise ValueError(f"field components must be {shape}")
+        if not (np.all(np.isfinite(dx)) and np.all(np.isfinite(dy))):
+            raise ValueError("field contains non-finite values")
+        dx = dx.copy()
+        dy = dy.copy()
+        dx.setflags(write=False)
+        dy.setflags(write=False)
+        object.__setattr__(self, "_dx", dx)
+        object.__setattr__(self, "_dy", dy)
+        object.__setattr__(self, "_ddx", None)
+        object.__setattr__(self, "_ddy", None)
+
+    def __setattr__(self, name, value):
+        raise AttributeError("MotionField is immutable")
+
+    def _host(self):
+        if self._dx is None:
+            dx = self._ddx.cpu().numpy()
+            dy = self._ddy.cpu().numpy()
+            if not (np.all(np.isfinite(dx)) and np.all(np.isfinite(dy))):
+                raise ValueError("field contains non-finite values")
+            dx.setflags(write=False)
+            dy.setflags(write=False)
+            object.__setattr__(self, "_dx", dx)
+            object.__setattr__(self, "_dy", dy)
+
+    @property
+    def dx(self) -> np.ndarray:
+        self._host()
+        return self._dx
+
+    @property
+    def dy(self) -> np.ndarray:
+        self._host()
+        return self._dy
+
+    def device(self):
+        """(dx, dy) as CUDA float64 tensors."""
+        if self._ddx is None:
+            import torch
+            object.__setattr__(self, "_ddx", torch.from_numpy(np.array(self._dx)).cuda())
+            object.__setattr__(self, "_ddy", torch.from_numpy(np.array(self._dy)).cuda())
+        return self._ddx, self._ddy
+
+    def magnitude(self) -> np.ndarray:
+        return np.hypot(self.dx, self.dy)
+
+
+def auto_scales(width: int, height: int) -> int:
+    """Pyramid depth whose coarsest level keeps both sides >= 16 (optflow.py:96-104)."""
+    out = C.c_int()
+    _lib.check(_lib.load().ft_auto_scales(int(width), int(height), C.byref(out)))
+    return out.value
+
+
+def compute_flow(prev: Frame, curr: Frame, params: FlowParams = FlowParams(),
+                 energy_trace: list | None = None) -> MotionField:
+    """Coarse-to-fine TV-L1 from prev to curr (optflow.py:217-253).
+
+    Both frames are expected to be structure-texture preprocessed.
+    `energy_trace` (a diagnostic) is not supported
+    on the device path.
+    """
+    import torch
+
+    if energy_trace is not None:
+        raise NotImplementedError("energy_trace is a CPU diagnostic, not part of the device path")
+    if (prev.width, prev.height) != (curr.width, curr.height):
+        raise ValueError(f"frame sizes differ: {prev.width}x{prev.height} vs "
+                         f"{curr.width}x{curr.height}")
+    if prev.width < 2 or prev.height < 2:
+        raise ValueError("frames must be at least 2x2")
+    a = prev.device()
+    b = curr.device()
+    dx = torch.empty_like(a)
+    dy = torch.empty_like(a)
+    prm = _lib.flow_params_struct(params)
+    _lib.check(_lib.load().ft_compute_flow(_lib.ctx(), _lib.ptr(a), _lib.ptr(b), prev.width,
+                                           prev.height, C.byref(prm), _lib.ptr(dx),
+                                           _lib.ptr(dy)))
+    return MotionField(prev.width, prev.height, dx, dy, frame_index=curr.index)

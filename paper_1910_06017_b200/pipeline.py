@@ -1,0 +1,191 @@
+"""Frame in, tracks out: the per-frame step the reference specifies but does
+not ship (composition per SURVEY.md section 8 A16).
+
+`Tracker` advances `n_streams` independent video streams in lockstep; one
+call = one frame for every stream, executed as a single CUDA graph in
+libomnitrack (ingest -> pyramid -> ROF structure-texture -> flow pyramid ->
+TV-L1 -> predict -> score gate -> IoU/Hungarian match -> update).  Per
+stream the semantics are exactly:
+
+1. L = select_level(W, H); st = structure_texture(build_pyramid(f, L+1)[L]).
+2. dets = filter_detections(dets, min_score) when the detector produced a
+   result this frame; `None` means no result (coast).
+3. first frame: every kept detection spawns a track.
+4. otherwise field = compute_flow(prev_st, st); every Active track's box is
+   replaced by its prediction (kept when predict returns None).
+5. coast frames stop here; else match the Active tracks that have a
+   prediction and update the full scene (Lost tracks never re-enter and
+   their ids are never reused).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from .optflow import FlowParams
+from .track import ACTIVE, LOST, SceneObject
+
+
+class Tracker:
+    """Multi-stream B200 tracker (frame in, tracks out)."""
+
+    def __init__(self, width: int, height: int, n_streams: int = 1,
+                 flow_params: FlowParams = FlowParams(), gate: float = 0.3,
+                 min_score: float = 0.5, detection_blend: float = 1.0,
+                 max_tracks: int = 512, max_dets: int = 512,
+                 smoothing_weight: float = 12.0, blend: float = 0.05,
+                 rof_iterations: int = 40, device: int | None = None):
+        import torch
+
+        self.width, self.height, self.n_streams = int(width), int(height), int(n_streams)
+        self.max_tracks, self.max_dets = int(max_tracks), int(max_dets)
+        self.flow_params = flow_params
+        self._lib = _lib.load()
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self._ctx = _lib.ctx(self.device)
+        cfg = _lib.ft_tracker_config(
+            self.width, self.height, self.n_streams, self.max_tracks, self.max_dets,
+            int(rof_iterations), float(gate), float(min_score), float(detection_blend),
+            float(smoothing_weight), float(blend), _lib.flow_params_struct(flow_params))
+        h = C.c_void_p()
+        _lib.check(self._lib.ft_tracker_create(self._ctx, C.byref(cfg), C.byref(h)))
+        self._h = h.value
+        # pinned staging owned by the library, viewed as numpy
+        pl, pd, pn = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        _lib.check(self._lib.ft_tracker_input_buffers(self._h, C.byref(pl), C.byref(pd),
+                                                      C.byref(pn)))
+        S = self.n_streams
+        self.luma_in = np.ctypeslib.as_array(
+            (C.c_uint8 * (S * self.height * self.width)).from_address(pl.value)
+        ).reshape(S, self.height, self.width)
+        self.dets_in = np.frombuffer(
+            (C.c_uint8 * (S * self.max_dets * _lib.DET_DTYPE.itemsize)).from_address(pd.value),
+            dtype=_lib.DET_DTYPE).reshape(S, self.max_dets)
+        self.ndets_in = np.ctypeslib.as_array((C.c_int32 * S).from_address(pn.value))
+        self._out = np.zeros((S, 2 * self.max_tracks), dtype=_lib.TRACK_DTYPE)
+        self._nout = np.zeros(S, dtype=np.int32)
+        self._labels: dict = {}
+        self._label_names: list = []
+        self._tombstones = [[] for _ in range(S)]
+        self._frame = 0
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.ft_tracker_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def reset(self):
+        _lib.check(self._lib.ft_tracker_reset(self._h))
+        self._tombstones = [[] for _ in range(self.n_streams)]
+
+    # ------------------------------------------------------------------
+    def _label_ref(self, label: str) -> int:
+        ref = self._labels.get(label)
+        if ref is None:
+            ref = self._labels[label] = len(self._label_names)
+            self._label_names.append(label)
+        return ref
+
+    def _stage(self, frames, detections):
+        S = self.n_streams
+        frames = np.asarray(frames, dtype=np.uint8)
+        if frames.ndim == 2:
+            frames = frames[None]
+        if frames.shape != (S, self.height, self.width):
+            raise ValueError(f"frames must be {(S, self.height, self.width)}, got {frames.shape}")
+        self.luma_in[...] = frames
+        if detections is None:
+            detections = [None] * S
+        if len(detections) != S:
+            raise ValueError(f"need one detection list (or None) per stream ({S})")
+        for s, dets in enumerate(detections):
+            if dets is None:
+                self.ndets_in[s] = -1
+                continue
+            if isinstance(dets, np.ndarray) and dets.dtype == _lib.DET_DTYPE:
+                n = len(dets)
+                if n > self.max_dets:
+                    raise ValueError(f"{n} detections exceed max_dets={self.max_dets}")
+                self.dets_in[s, :n] = dets
+                self.ndets_in[s] = n
+                continue
+            n = len(dets)
+            if n > self.max_dets:
+                raise ValueError(f"{n} detections exceed max_dets={self.max_dets}")
+            rec = self.dets_in[s]
+            for j, d in enumerate(dets):
+                rec[j] = (d.class_id, self._label_ref(d.label), d.score, *d.box)
+            self.ndets_in[s] = n
+
+    def step_records(self, frames, frame_index: int, detections=None):
+        """One frame for every stream; returns a list (per stream) of
+        TRACK_DTYPE record arrays: the active tracks in scene order followed
+        by the tracks that turned Lost this frame."""
+        self._stage(frames, detections)
+        _lib.check(self._lib.ft_tracker_step(
+            self._h, _lib.ptr(self.luma_in), int(frame_index), _lib.ptr(self.dets_in),
+            _lib.ptr(self.ndets_in), _lib.ptr(self._out), _lib.ptr(self._nout)))
+        self._frame = frame_index
+        return [self._out[s, :self._nout[s]] for s in range(self.n_streams)]
+
+    def step(self, frames, frame_index: int, detections=None):
+        """One frame for every stream; returns, per stream, the full scene
+        list (SceneObjects, Lost tombstones included, id order) exactly like
+        the reference's scene after `update`."""
+        recs = self.step_records(frames, frame_index, detections)
+        scenes = []
+        for s, r in enumerate(recs):
+            active, newly_lost = [], []
+            for row in r:
+                obj = self._obj(row)
+                (active if obj.state == ACTIVE else newly_lost).append(obj)
+            self._tombstones[s].extend(newly_lost)
+            scene = sorted(self._tombstones[s] + active, key=lambda o: o.id)
+            scenes.append(scene)
+        return scenes
+
+    def _obj(self, row) -> SceneObject:
+        lr = int(row["label_ref"])
+        label = self._label_names[lr] if 0 <= lr < len(self._label_names) else ""
+        return SceneObject(id=int(row["id"]), class_id=int(row["class_id"]), label=label,
+                           box=(float(row["x"]), float(row["y"]), float(row["w"]),
+                                float(row["h"])),
+                           state=ACTIVE if row["state"] == 1 else LOST,
+                           born_at=int(row["born_at"]), last_seen=int(row["last_seen"]),
+                           score=float(row["score"]),
+                           lost_at=None if row["lost_at"] < 0 else int(row["lost_at"]))
+
+    # ------------------------------------------------------------------ device I/O
+    def step_device(self, d_luma, frame_index: int, d_dets, d_ndets):
+        """Step with inputs resident in device memory (torch tensors): no
+        host copies, no synchronisation (kernel-only timing)."""
+        _lib.check(self._lib.ft_tracker_step_device(self._h, _lib.ptr(d_luma), int(frame_index),
+                                                    _lib.ptr(d_dets), _lib.ptr(d_ndets)))
+
+    def read(self):
+        _lib.check(self._lib.ft_tracker_read(self._h, _lib.ptr(self._out), _lib.ptr(self._nout)))
+        return [self._out[s, :self._nout[s]] for s in range(self.n_streams)]
+
+    def field(self, stream: int = 0):
+        """(dx, dy) of the last step's motion field for one stream (host copy)."""
+        pdx, pdy, w, h = C.c_void_p(), C.c_void_p(), C.c_int(), C.c_int()
+        _lib.check(self._lib.ft_tracker_field(self._h, stream, C.byref(pdx), C.byref(pdy),
+                                              C.byref(w), C.byref(h)))
+        dx = np.empty((h.value, w.value), dtype=np.float64)
+        dy = np.empty_like(dx)
+        _lib.check(self._lib.ft_tracker_read_field(self._h, stream, _lib.ptr(dx), _lib.ptr(dy)))
+        return dx, dy
+
+    def launches(self) -> int:
+        c = C.c_int64()
+        _lib.check(self._lib.ft_tracker_launches(self._h, C.byref(c)))
+        return c.value
+

@@ -1,0 +1,240 @@
+"""Device parity: libomnitrack (through the drop-in Python API and the C
+ABI) against the golden fixtures produced by the live reference and against
+the CPU oracle.  Bit-exact everywhere: the kernels restate the reference's
+IEEE operation order (compiled with -fmad=false), so flow, boxes, ids and
+assignments must be identical, not merely within the 1e-3 px tolerance
+north_star allows (FLOW_TOL below is asserted as well, as the contract)."""
+import numpy as np
+import pytest
+
+from tests.goldutil import predict_field, scene_rows, step_dets
+
+pytestmark = pytest.mark.gpu
+
+FLOW_TOL = 1e-3  # px, north_star tolerance for flow / boxes
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("gpu tests need a CUDA device")
+    import paper_1910_06017_b200 as P
+    from paper_1910_06017_b200 import assoc, imaging, optflow, pipeline, track
+    P.imaging, P.optflow, P.track, P.assoc, P.pipeline = imaging, optflow, track, assoc, pipeline
+    return P
+
+
+def test_gray8_and_pyramid(pkg, golden):
+    z = golden("imaging.npz")
+    im = pkg.imaging
+    for k in range(4):
+        u8 = z[f"pyr{k}_in"]
+        want = [z[key] for key in sorted(k2 for k2 in z.files if k2.startswith(f"pyr{k}_l"))]
+        f = im.Frame.from_gray8(u8)
+        assert np.array_equal(f.data, want[0])
+        pyr = im.build_pyramid(f, len(want))
+        for lv, w in zip(pyr.levels, want):
+            assert np.array_equal(lv.data, w)
+
+
+def test_pyramid_errors(pkg):
+    im = pkg.imaging
+    f = im.Frame.from_array(np.zeros((5, 5)))
+    with pytest.raises(ValueError, match="at least 2x2"):
+        im.build_pyramid(f, 3)
+
+
+def test_structure_texture(pkg, golden):
+    z = golden("imaging.npz")
+    im = pkg.imaging
+    for k in range(4):
+        wt, bl, it = z[f"st{k}_prm"]
+        f = im.Frame.from_gray8(z[f"st{k}_in"])
+        got = im.structure_texture(f, wt, bl, int(it)).data
+        assert np.array_equal(got, z[f"st{k}_out"]), k
+
+
+def test_rof_denoise_matches_oracle(pkg):
+    from oracle import ftoracle as O
+    rng = np.random.default_rng(4)
+    img = rng.random((37, 53))
+    got = pkg.imaging.rof_denoise(img, 12.0, 40)
+    assert np.array_equal(got, O.rof(img, 12.0, 40))
+
+
+def test_flow_bit_exact(pkg, golden):
+    z = golden("flow.npz")
+    im, of = pkg.imaging, pkg.optflow
+    for k in range(5):
+        w, h, sc, wp, it = (int(v) for v in z[f"f{k}_prm"])
+        prm = of.FlowParams(warps_per_level=wp, iterations_per_warp=it,
+                            pyramid_scales=None if sc < 0 else sc)
+        a = im.Frame.from_array(z[f"f{k}_sta"], 0)
+        b = im.Frame.from_array(z[f"f{k}_stb"], 1)
+        fld = of.compute_flow(a, b, prm)
+        assert fld.frame_index == 1
+        assert np.abs(fld.dx - z[f"f{k}_dx"]).max() <= FLOW_TOL
+        assert np.abs(fld.dy - z[f"f{k}_dy"]).max() <= FLOW_TOL
+        assert np.array_equal(fld.dx, z[f"f{k}_dx"]), (k, np.abs(fld.dx - z[f"f{k}_dx"]).max())
+        assert np.array_equal(fld.dy, z[f"f{k}_dy"]), k
+
+
+def test_flow_sd_tiled_matches_oracle(pkg):
+    """Full SD-width frame (multi-tile, halo exchange) vs the oracle with light
+    params; the oracle's cost bounds the size."""
+    from oracle import ftoracle as O
+    from paper_1910_06017_b200.synth import make_sequence
+    frames, _ = make_sequence(200, 136, 6, 2, seed=3)
+    sa = O.structure_texture(O.gray8_to_unit(frames[0]))
+    sb = O.structure_texture(O.gray8_to_unit(frames[1]))
+    prm_o = O.FlowParams(warps_per_level=2, iterations_per_warp=11, pyramid_scales=3)
+    want = O.compute_flow(sa, sb, prm_o)
+    of, im = pkg.optflow, pkg.imaging
+    prm = of.FlowParams(warps_per_level=2, iterations_per_warp=11, pyramid_scales=3)
+    fld = of.compute_flow(im.Frame.from_array(sa), im.Frame.from_array(sb), prm)
+    assert np.array_equal(fld.dx, want[0])
+    assert np.array_equal(fld.dy, want[1])
+
+
+def test_zero_motion_full_size(pkg):
+    """Size-independent property at SD (720x576, default params): identical
+    frames give an exactly zero field."""
+    from paper_1910_06017_b200.synth import make_sequence
+    frames, _ = make_sequence(720, 576, 10, 1, seed=5)
+    im, of = pkg.imaging, pkg.optflow
+    st = im.structure_texture(im.Frame.from_gray8(frames[0]))
+    fld = of.compute_flow(st, st)
+    assert np.abs(fld.dx).max() == 0.0 and np.abs(fld.dy).max() == 0.0
+
+
+def test_predict_bit_exact(pkg, golden):
+    z = golden("predict.npz")
+    tr, of = pkg.track, pkg.optflow
+    for k in range(4):
+        fw, fh, lvl = (int(v) for v in z[f"p{k}_meta"])
+        lw, lh = fw >> lvl, fh >> lvl
+        dx, dy = predict_field(k, lw, lh)
+        fld = of.MotionField(lw, lh, dx, dy)
+        objs = [tr.SceneObject(id=i, class_id=0, label="x", box=tuple(b))
+                for i, b in enumerate(z[f"p{k}_boxes"])]
+        got = tr.predict(objs, fld, lvl, (fw, fh))
+        for g, w in zip(got, z[f"p{k}_out"]):
+            if g is None:
+                assert np.isnan(w).all()
+            else:
+                assert np.array_equal(np.array(g), w)
+    objs = [tr.SceneObject(id=0, class_id=0, label="a", box=(10, 10, 20, 20))]
+    fld = of.MotionField(64, 64, np.full((64, 64), 3.0), np.full((64, 64), -2.0))
+    assert tr.predict(objs, fld, 0, (64, 64))[0] == (13.0, 8.0, 20.0, 20.0)
+    lost = [tr.SceneObject(id=0, class_id=0, label="a", box=(1, 1, 2, 2), state=tr.LOST)]
+    with pytest.raises(ValueError):
+        tr.predict(lost, fld, 0, (64, 64))
+
+
+def test_iou_hungarian_match(pkg, golden):
+    z = golden("assoc.npz")
+    a = pkg.assoc
+    got = a.iou_matrix(z["iou_a"], z["iou_b"])
+    assert np.array_equal(got, z["iou_ab"])
+    assert a.iou((0, 0, 10, 10), (5, 0, 10, 10)) == 1 / 3
+    with pytest.raises(ValueError):
+        a.iou((0, 0, 0, 1), (0, 0, 1, 1))
+    for k in range(40):
+        forb = a.FORBIDDEN_COST if bool(z[f"h{k}_forb"][0]) else None
+        assert a.hungarian(z[f"h{k}_cost"], forbidden=forb) == \
+            [tuple(p) for p in z[f"h{k}_pairs"].tolist()], k
+    assert a.hungarian([[1.0, 2.0], [2.0, 4.0]]) == [(0, 1), (1, 0)]
+    assert a.hungarian([[3.0], [1.0]]) == [(1, 0)]
+    assert a.hungarian(np.ones((3, 2))) == [(0, 0), (1, 1)]
+    assert a.hungarian(np.zeros((0, 4))) == []
+    with pytest.raises(ValueError):
+        a.hungarian([[np.inf]])
+    tr = pkg.track
+    from paper_1910_06017_b200.detect import Detection
+    for k in range(3):
+        objs = [tr.SceneObject(id=i, class_id=int(c), label="t", box=tuple(b))
+                for i, (b, c) in enumerate(zip(z[f"m{k}_tb"], z[f"m{k}_tc"]))]
+        dets = [Detection(class_id=int(c), label="d", score=0.9, box=tuple(b))
+                for b, c in zip(z[f"m{k}_db"], z[f"m{k}_dc"])]
+        asg = a.match(objs, dets, 0.3)
+        assert [(i, j) for i, j, _ in asg.pairs] == [tuple(p) for p in z[f"m{k}_pairs"].tolist()]
+        assert np.array_equal(np.array([s for _, _, s in asg.pairs]), z[f"m{k}_ious"])
+        assert list(asg.unmatched_scene) == z[f"m{k}_um_s"].tolist()
+        assert list(asg.unmatched_detections) == z[f"m{k}_um_d"].tolist()
+
+
+def test_hungarian_large_vs_oracle(pkg):
+    from oracle import ftoracle as O
+    rng = np.random.default_rng(9)
+    for m, n in [(100, 100), (150, 90), (60, 200), (300, 300)]:
+        c = rng.random((m, n))
+        c[rng.random((m, n)) < 0.9] = O.FORBIDDEN
+        assert pkg.assoc.hungarian(c, O.FORBIDDEN) == O.hungarian(c, O.FORBIDDEN)
+        c = rng.integers(0, 4, (m, n)).astype(np.float64)  # tie-heavy
+        assert pkg.assoc.hungarian(c) == O.hungarian(c)
+
+
+def test_update_lifecycle(pkg):
+    tr, a = pkg.track, pkg.assoc
+    from paper_1910_06017_b200.detect import Detection
+    d = [Detection(1, "a", 0.9, (0.0, 0.0, 5.0, 5.0)), Detection(2, "b", 0.8, (9.0, 9.0, 3.0, 3.0))]
+    s = tr.update([], a.Assignment((), (), (0, 1)), d, 0)
+    assert [o.id for o in s] == [0, 1] and s[1].label == "b"
+    s = tr.update(s, a.Assignment(((1, 0, 0.5),), (0,), ()),
+                  [Detection(2, "b", 0.7, (9.5, 9.0, 3.0, 3.0))], 1)
+    assert s[0].state == tr.LOST and s[0].lost_at == 1
+    assert s[1].box == (9.5, 9.0, 3.0, 3.0) and s[1].last_seen == 1 and s[1].score == 0.7
+    s = tr.update(s, a.Assignment((), (), ()), d, 2)
+    assert [o.id for o in s] == [0, 1, 2, 3]
+    with pytest.raises(ValueError):
+        tr.update(s, a.Assignment(((0, 0, 1.0),), (), ()), d, 3)
+    with pytest.raises(IndexError):
+        tr.update(s, a.Assignment(((9, 0, 1.0),), (), ()), d, 3)
+    # blend < 1 (track.py:118-123)
+    s2 = tr.update([tr.SceneObject(0, 1, "a", (0, 0, 4, 4))], a.Assignment(((0, 0, 1.0),), (), ()),
+                   [Detection(1, "a", 0.5, (2.0, 2.0, 8.0, 8.0))], 5, detection_blend=0.25)
+    assert s2[0].box == tuple(0.25 * dv + 0.75 * ov for dv, ov in zip((2, 2, 8, 8), (0, 0, 4, 4)))
+
+
+@pytest.mark.parametrize("name", ["s0", "s1", "s2"])
+def test_tracker_step_matches_reference(pkg, golden, name):
+    """End-to-end frame-in/tracks-out through Tracker vs the reference
+    composition (tests/golden/make_golden.py:ref_step)."""
+    z = golden(f"step_{name}.npz")
+    W, H, sc, wp, it = (int(v) for v in z["prm"])
+    prm = pkg.optflow.FlowParams(warps_per_level=wp, iterations_per_warp=it,
+                                 pyramid_scales=None if sc < 0 else sc)
+    trk = pkg.pipeline.Tracker(W, H, n_streams=1, flow_params=prm, max_tracks=64, max_dets=64)
+    frames = z["frames"]
+    for t in range(frames.shape[0]):
+        scene = trk.step(frames[t], t, [step_dets(z, t)])[0]
+        assert np.array_equal(scene_rows(scene), z[f"scene{t}"]), (name, t)
+    trk.close()
+
+
+def test_tracker_multistream_matches_oracle(pkg):
+    """Several independent streams in one lockstep tracker: each stream's
+    output equals the oracle run on that stream alone (stream isolation)."""
+    from oracle import ftoracle as O
+    from paper_1910_06017_b200.synth import make_sequence
+    S, W, H, T = 3, 128, 96, 5
+    prm = pkg.optflow.FlowParams(warps_per_level=2, iterations_per_warp=9)
+    oprm = O.FlowParams(warps_per_level=2, iterations_per_warp=9)
+    seqs = [make_sequence(W, H, 4 + s, T, seed=40 + s, det_every=2, scale_change=True)
+            for s in range(S)]
+    trk = pkg.pipeline.Tracker(W, H, n_streams=S, flow_params=prm, max_tracks=64, max_dets=64)
+    states = [O.StreamState() for _ in range(S)]
+    for t in range(T):
+        frames = np.stack([seqs[s][0][t] for s in range(S)])
+        dets = [seqs[s][1][t] for s in range(S)]
+        scenes = trk.step(frames, t, dets)
+        for s in range(S):
+            od = None if dets[s] is None else [O.Det(d.class_id, d.label, d.score, d.box)
+                                                for d in dets[s]]
+            O.step(states[s], frames[s], t, od, oprm)
+            assert np.array_equal(scene_rows(scenes[s]), scene_rows(states[s].tracks)), (s, t)
+    dx, dy = trk.field(1)
+    assert dx.shape == (H, W)
+    assert trk.launches() > 0
+    trk.close()

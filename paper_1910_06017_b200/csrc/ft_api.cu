@@ -205,7 +205,9 @@ int ft_ctx_destroy(ft_ctx *ctx) {
 
 int ft_ctx_set_stream(ft_ctx *ctx, void *stream) {
   if (!ctx) return fail(FT_EINVAL, "ctx is NULL");
-  ctx->stream = stream ? (cudaStream_t)stream : ctx->own;
+  // verbatim, like the CUDA runtime: NULL is the legacy default stream
+  // (torch's default stream reports handle 0)
+  ctx->stream = (cudaStream_t)stream;
   return FT_OK;
 }
 
@@ -469,6 +471,20 @@ int ft_update(ft_ctx *ctx, const int64_t *h_ids, const int32_t *h_state, const d
 // ============================================================ tracker
 struct ft_tracker {
   ft_ctx *ctx = nullptr;
+  // the tracker's own capture/launch stream, joined to the caller's stream
+  // (ctx->stream) by events at entry and exit of every call
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  int join_in() {
+    FT_CUDA_TRY(cudaEventRecord(ev_in, ctx->stream));
+    FT_CUDA_TRY(cudaStreamWaitEvent(stream, ev_in, 0));
+    return FT_OK;
+  }
+  int join_out() {
+    FT_CUDA_TRY(cudaEventRecord(ev_out, stream));
+    FT_CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ev_out, 0));
+    return FT_OK;
+  }
   ft_tracker_config cfg{};
   int S = 0, W = 0, H = 0, L = 0, PW = 0, PH = 0, scales = 0;
   int64_t P = 0;  // processing-level pixels
@@ -575,7 +591,7 @@ struct ft_tracker {
 
   int run(bool has_prev, const uint8_t *luma, const ft_det *dets, const int32_t *in,
           bool host_io) {
-    cudaStream_t s = ctx->stream;
+    cudaStream_t s = stream;
     GraphKey key{has_prev ? 1 : 0, host_io ? nullptr : luma, host_io ? nullptr : dets,
                  host_io ? nullptr : in};
     auto it = graphs.find(key);
@@ -626,6 +642,9 @@ int ft_tracker_create(ft_ctx *ctx, const ft_tracker_config *cfg, ft_tracker **ou
   std::unique_ptr<ft_tracker> t(new ft_tracker());
   t->ctx = ctx;
   t->cfg = *cfg;
+  FT_CUDA_TRY(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking));
+  FT_CUDA_TRY(cudaEventCreateWithFlags(&t->ev_in, cudaEventDisableTiming));
+  FT_CUDA_TRY(cudaEventCreateWithFlags(&t->ev_out, cudaEventDisableTiming));
   t->S = cfg->n_streams;
   t->W = cfg->width;
   t->H = cfg->height;
@@ -659,8 +678,6 @@ int ft_tracker_create(ft_ctx *ctx, const ft_tracker_config *cfg, ft_tracker **ou
   FT_TRY(t->alloc(&t->d_fchain, (size_t)S * t->geo.total));
   FT_TRY(t->alloc(&t->d_dx, (size_t)S * P));
   FT_TRY(t->alloc(&t->d_dy, (size_t)S * P));
-  FT_CUDA_TRY(cudaMemset(t->d_dx, 0, (size_t)S * P * 8));
-  FT_CUDA_TRY(cudaMemset(t->d_dy, 0, (size_t)S * P * 8));
   FT_TRY(t->alloc(&t->d_dets, (size_t)S * cfg->max_dets));
   FT_TRY(t->alloc(&t->d_in, (size_t)S + 1));
   FT_TRY(t->alloc(&t->d_out, (size_t)S * 2 * cfg->max_tracks));
@@ -713,12 +730,15 @@ int ft_tracker_create(ft_ctx *ctx, const ft_tracker_config *cfg, ft_tracker **ou
 int ft_tracker_reset(ft_tracker *t) {
   if (!t) return fail(FT_EINVAL, "tracker is NULL");
   DeviceGuard g(t->ctx->device);
-  FT_CUDA_TRY(cudaStreamSynchronize(t->ctx->stream));
+  FT_TRY(t->join_in());
   const int S = t->S;
-  FT_CUDA_TRY(cudaMemset(t->T.n_active, 0, S * 4));
-  FT_CUDA_TRY(cudaMemset(t->T.next_id, 0, S * 8));
-  FT_CUDA_TRY(cudaMemset(t->T.n_lost, 0, S * 4));
-  FT_CUDA_TRY(cudaMemset(t->T.overflow, 0, S * 4));
+  FT_CUDA_TRY(cudaMemsetAsync(t->T.n_active, 0, S * 4, t->stream));
+  FT_CUDA_TRY(cudaMemsetAsync(t->T.next_id, 0, S * 8, t->stream));
+  FT_CUDA_TRY(cudaMemsetAsync(t->T.n_lost, 0, S * 4, t->stream));
+  FT_CUDA_TRY(cudaMemsetAsync(t->T.overflow, 0, S * 4, t->stream));
+  FT_CUDA_TRY(cudaMemsetAsync(t->d_dx, 0, (size_t)S * t->P * 8, t->stream));
+  FT_CUDA_TRY(cudaMemsetAsync(t->d_dy, 0, (size_t)S * t->P * 8, t->stream));
+  FT_CUDA_TRY(cudaStreamSynchronize(t->stream));
   t->frames_seen = 0;
   return FT_OK;
 }
@@ -726,7 +746,7 @@ int ft_tracker_reset(ft_tracker *t) {
 int ft_tracker_destroy(ft_tracker *t) {
   if (!t) return FT_OK;
   DeviceGuard g(t->ctx->device);
-  cudaStreamSynchronize(t->ctx->stream);
+  cudaStreamSynchronize(t->stream);
   for (auto &kv : t->graphs) cudaGraphExecDestroy(kv.second.exec);
   for (void *p : t->allocs) cudaFree(p);
   flow_work_free(t->fw);
@@ -735,6 +755,9 @@ int ft_tracker_destroy(ft_tracker *t) {
   cudaFreeHost(t->h_in);
   cudaFreeHost(t->h_out);
   cudaFreeHost(t->h_nout);
+  if (t->ev_in) cudaEventDestroy(t->ev_in);
+  if (t->ev_out) cudaEventDestroy(t->ev_out);
+  if (t->stream) cudaStreamDestroy(t->stream);
   delete t;
   return FT_OK;
 }
@@ -759,8 +782,9 @@ int ft_tracker_step(ft_tracker *t, const uint8_t *luma, int frame, const ft_det 
   if (dets && dets != t->h_dets) std::memcpy(t->h_dets, dets, (size_t)S * D * sizeof(ft_det));
   if (n_dets != t->h_in + 1) std::memcpy(t->h_in + 1, n_dets, (size_t)S * 4);
   t->h_in[0] = frame;
+  FT_TRY(t->join_in());
   FT_TRY(t->run(t->frames_seen > 0, nullptr, nullptr, nullptr, true));
-  FT_CUDA_TRY(cudaStreamSynchronize(t->ctx->stream));
+  FT_CUDA_TRY(cudaStreamSynchronize(t->stream));
   t->frames_seen++;
   return read_staged(t, out, n_out);
 }
@@ -772,7 +796,8 @@ int ft_tracker_step_device(ft_tracker *t, const uint8_t *d_luma, int frame, cons
   // gather the caller's device inputs into the tracker's fixed input buffers
   // (D2D, ~HBM speed) so one captured graph serves every step; the frame
   // index travels in d_in[0] (pageable source: staged before return).
-  cudaStream_t s = t->ctx->stream;
+  cudaStream_t s = t->stream;
+  FT_TRY(t->join_in());
   const int32_t fr = frame;
   FT_CUDA_TRY(cudaMemcpyAsync(t->d_in, &fr, 4, cudaMemcpyHostToDevice, s));
   FT_CUDA_TRY(cudaMemcpyAsync(t->d_in + 1, d_n_dets, (size_t)t->S * 4, cudaMemcpyDeviceToDevice, s));
@@ -782,13 +807,14 @@ int ft_tracker_step_device(ft_tracker *t, const uint8_t *d_luma, int frame, cons
                               cudaMemcpyDeviceToDevice, s));
   FT_TRY(t->run(t->frames_seen > 0, t->d_luma, t->d_dets, t->d_in, false));
   t->frames_seen++;
-  return FT_OK;
+  return t->join_out();
 }
 
 int ft_tracker_read(ft_tracker *t, ft_track *out, int32_t *n_out) {
   if (!t) return fail(FT_EINVAL, "tracker is NULL");
   DeviceGuard g(t->ctx->device);
-  cudaStream_t s = t->ctx->stream;
+  cudaStream_t s = t->stream;
+  FT_TRY(t->join_in());
   FT_CUDA_TRY(cudaMemcpyAsync(t->h_out, t->d_out, (size_t)t->S * 2 * t->cfg.max_tracks * sizeof(ft_track),
                               cudaMemcpyDeviceToHost, s));
   FT_CUDA_TRY(cudaMemcpyAsync(t->h_nout, t->d_nout, (size_t)2 * t->S * 4, cudaMemcpyDeviceToHost, s));
@@ -827,7 +853,8 @@ int ft_tracker_field(ft_tracker *t, int stream, const double **dx, const double 
 int ft_tracker_read_field(ft_tracker *t, int stream, double *h_dx, double *h_dy) {
   if (!t || stream < 0 || stream >= t->S) return fail(FT_EINVAL, "bad stream");
   DeviceGuard g(t->ctx->device);
-  cudaStream_t s = t->ctx->stream;
+  cudaStream_t s = t->stream;
+  FT_TRY(t->join_in());
   const size_t nb = (size_t)t->P * 8;
   if (h_dx)
     FT_CUDA_TRY(cudaMemcpyAsync(h_dx, t->d_dx + (int64_t)stream * t->P, nb, cudaMemcpyDeviceToHost, s));
@@ -841,11 +868,12 @@ int ft_tracker_profile_pd(ft_tracker *t, int reps, double *ms_per_launch, double
                           int *iters_per_launch) {
   if (!t || !ms_per_launch || reps < 1) return fail(FT_EINVAL, "bad argument");
   DeviceGuard g(t->ctx->device);
-  FT_CUDA_TRY(cudaStreamSynchronize(t->ctx->stream));
+  FT_TRY(t->join_in());
+  FT_CUDA_TRY(cudaStreamSynchronize(t->stream));
   FlowParamsD p{t->cfg.flow.data_weight, t->cfg.flow.time_step, t->cfg.flow.huber_epsilon,
                 t->cfg.flow.warps_per_level, t->cfg.flow.iterations_per_warp};
   int iters = 0;
-  FT_TRY(profile_pd(t->fw, t->PW, t->PH, t->S, p, reps, t->ctx->stream, ms_per_launch, &iters));
+  FT_TRY(profile_pd(t->fw, t->PW, t->PH, t->S, p, reps, t->stream, ms_per_launch, &iters));
   // compulsory HBM bytes of one launch: read 11 planes (8 state + gx gy
   // rho0) and write 8 state planes once per pixel
   if (bytes_per_launch) *bytes_per_launch = 152.0 * (double)t->P * t->S;

@@ -702,6 +702,7 @@ int ft_tracker_create(ft_ctx *ctx, const ft_tracker_config *cfg, ft_tracker **ou
   FT_TRY(t->alloc(&T.last_seen, (size_t)S * C));
   FT_TRY(t->alloc(&T.box, (size_t)S * C * 4));
   FT_TRY(t->alloc(&T.score, (size_t)S * C));
+  FT_TRY(t->alloc(&T.pmean, (size_t)S * C * 2));
   FT_TRY(t->alloc(&T.n_active, (size_t)S));
   FT_TRY(t->alloc(&T.n_cand, (size_t)S));
   FT_TRY(t->alloc(&T.cand, (size_t)S * C));

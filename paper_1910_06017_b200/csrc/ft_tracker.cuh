@@ -17,7 +17,7 @@ struct TrackerDev {
   double gate, min_score, blend;
   int64_t *id, *next_id;
   int32_t *cls, *label, *born, *last_seen;
-  double *box, *score;
+  double *box, *score, *pmean;  // pmean: [cap][2] window means of predict
   int32_t *n_active, *n_cand, *cand, *n_kept, *kept, *row_col, *match_of, *n_lost, *overflow;
   unsigned char *valid, *det_used;
   double *scores, *cost;

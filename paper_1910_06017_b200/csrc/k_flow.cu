@@ -13,6 +13,7 @@
 //   state ping-pong st[2]           [8][nb][cap]  (u1 u2 b1 b2 p11 p12 p21 p22)
 // where b = "u bar" (optflow.py:173-174, :205-206).
 #include <algorithm>
+#include <cstdlib>
 
 #include "ft_internal.cuh"
 
@@ -162,26 +163,32 @@ __global__ void k_median(const double *__restrict__ a1, const double *__restrict
   o2[so + (int64_t)r * w + c] = median9(v);
 }
 
+StatePtrs state_ptrs(double *base, int nb, int64_t cap) {
+  StatePtrs s;
+  for (int k = 0; k < NST; ++k) s.p[k] = base + (int64_t)k * nb * cap;
+  return s;
+}
+
 // ------------------------------------------------------------------------
-// Primal-dual iterations, temporally blocked.
+// Primal-dual iterations, temporally blocked (optflow.py:178-208).
 //
-// A CTA owns a TWxTH tile of the level that overlaps its neighbours by `halo`
-// pixels on every side that is not an image border.  One iteration's
+// A CTA owns a TW x TH tile of the level that overlaps its neighbours by
+// `halo` pixels on every side that is not an image border.  One iteration's
 // dependency radius is 1 in each direction (dual step reads u-bar at x+1 and
 // y+1; primal step reads p at x-1 and y-1), so after `iters <= halo`
-// iterations the inner (TW-2*halo)x(TH-2*halo) region is exact and is
+// iterations the inner (TW-2*halo) x (TH-2*halo) region is exact and is
 // written back.  A tile that covers the whole level needs no halo and runs a
 // whole warp's iterations in one launch.
 //
-// Shared memory holds the fields read at a neighbour (b1 b2 p11 p12 p21 p22);
-// the pointwise fields (u, the gathered gradient, rho0 and the derived
-// threshold / inverse |grad|^2) live in registers of the owning thread.
+// Shared memory holds the fields read at a neighbour (b1 b2 p11 p12 p21 p22)
+// in [TH+2][TW+2] planes with a one-element apron, so every neighbour read
+// is an immediate offset from the thread's base address.  Each field is
+// updated in place: the dual step reads only its own p, the primal step only
+// its own u-bar, so two barriers per iteration suffice.  Pointwise fields
+// (u, the gathered gradient, rho0, the threshold, 1/|grad|^2 derived once per
+// launch) live in registers of the owning thread: thread (tx, ty) owns
+// columns tx + 32*cx (cx < TW/32) and rows ty + BY*k (k < PY).
 // ------------------------------------------------------------------------
-constexpr int kTW = 32;       // tile width  (one warp across)
-constexpr int kBY = 8;        // warps per CTA
-constexpr int kPY = 4;        // rows per thread (interleaved by kBY)
-constexpr int kTH = kBY * kPY;  // tile height
-
 struct PDArgs {
   StatePtrs in, out;
   const double *gx, *gy, *r0;
@@ -191,87 +198,115 @@ struct PDArgs {
   double tau, lam, sigma, shrink;  // shrink = 1/(1+sigma*eps)
 };
 
-__global__ void __launch_bounds__(kTW *kBY, 2) k_pd_tile(const PDArgs a) {
-  __shared__ double s_b1[kTH][kTW], s_b2[kTH][kTW];
-  __shared__ double s_p11[kTH][kTW], s_p12[kTH][kTW], s_p21[kTH][kTW], s_p22[kTH][kTW];
+// per-pixel border flags (global position, fixed for the launch)
+enum : unsigned { F_R = 1, F_D = 2, F_L = 4, F_LASTC = 8, F_U = 16, F_LASTR = 32, F_OK = 64 };
+
+template <int TW, int BY, int PY>
+struct PDGeom {
+  static constexpr int NX = TW / 32, TH = BY * PY, NP = NX * PY;
+  static constexpr int SP = TW + 2, SR = TH + 2, PLANE = SP * SR;
+  static constexpr size_t smem = 6 * PLANE * sizeof(double);
+};
+
+template <int TW, int BY, int PY, int MINB>
+__global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const PDArgs a) {
+  using G = PDGeom<TW, BY, PY>;
+  constexpr int NX = G::NX, TH = G::TH, NP = G::NP, SP = G::SP, PL = G::PLANE;
+  extern __shared__ __align__(16) double sm[];
+  double *const sb1 = sm, *const sb2 = sm + PL, *const sp11 = sm + 2 * PL;
+  double *const sp12 = sm + 3 * PL, *const sp21 = sm + 4 * PL, *const sp22 = sm + 5 * PL;
 
   const int W = a.w, H = a.h;
-  const int step_x = kTW - 2 * a.halo, step_y = kTH - 2 * a.halo;
+  const int step_x = TW - 2 * a.halo, step_y = TH - 2 * a.halo;
   const int ox = blockIdx.x * step_x - a.halo;
   const int oy = blockIdx.y * step_y - a.halo;
   const int64_t so = blockIdx.z * a.cap;
   const int tx = threadIdx.x, ty = threadIdx.y;
-  const int gc = ox + tx;
-  const bool cin = gc >= 0 && gc < W;
+  const int tid = ty * 32 + tx;
+  const int base = (ty + 1) * SP + tx + 1;  // apron offset (+1,+1)
+
+  // zero the apron ring once (read only by halo pixels, keeps them finite)
+  for (int k = tid; k < 2 * SP + 2 * TH; k += 32 * BY) {
+    int idx;
+    if (k < SP) idx = k;
+    else if (k < 2 * SP) idx = (TH + 1) * SP + (k - SP);
+    else if (k < 2 * SP + TH) idx = (k - 2 * SP + 1) * SP;
+    else idx = (k - 2 * SP - TH + 1) * SP + SP - 1;
+#pragma unroll
+    for (int f = 0; f < 6; ++f) sm[f * PL + idx] = 0.0;
+  }
 
   const double tl = a.tau * a.lam;
-  double u1[kPY], u2[kPY], gx[kPY], gy[kPY], r0[kPY], thr[kPY], ig2[kPY];
-  bool ok[kPY];
+  double u1[NP], u2[NP], gx[NP], gy[NP], r0[NP], thr[NP], ig2[NP];
+  unsigned fl[NP];
 
 #pragma unroll
-  for (int k = 0; k < kPY; ++k) {
-    const int lr = ty + kBY * k, gr = oy + lr;
-    const bool in = cin && gr >= 0 && gr < H;
-    const int64_t o = so + (int64_t)gr * W + gc;
-    double vu1 = 0, vu2 = 0, vb1 = 0, vb2 = 0, q11 = 0, q12 = 0, q21 = 0, q22 = 0;
-    double vgx = 0, vgy = 0, vr0 = 0;
-    if (in) {
-      vu1 = a.in.p[U1][o];
-      vu2 = a.in.p[U2][o];
-      if (a.first) {
-        vb1 = vu1;  // ub = u, p = 0 at the start of a warp (optflow.py:169-174)
-        vb2 = vu2;
-      } else {
-        vb1 = a.in.p[B1][o];
-        vb2 = a.in.p[B2][o];
-        q11 = a.in.p[P11][o];
-        q12 = a.in.p[P12][o];
-        q21 = a.in.p[P21][o];
-        q22 = a.in.p[P22][o];
+  for (int k = 0; k < PY; ++k) {
+#pragma unroll
+    for (int cx = 0; cx < NX; ++cx) {
+      const int q = k * NX + cx;
+      const int gc = ox + tx + 32 * cx, gr = oy + ty + BY * k;
+      const bool in = gc >= 0 && gc < W && gr >= 0 && gr < H;
+      const int64_t o = so + (int64_t)gr * W + gc;
+      double vu1 = 0, vu2 = 0, vb1 = 0, vb2 = 0, q11 = 0, q12 = 0, q21 = 0, q22 = 0;
+      double vgx = 0, vgy = 0, vr0 = 0;
+      if (in) {
+        vu1 = a.in.p[U1][o];
+        vu2 = a.in.p[U2][o];
+        if (a.first) {
+          vb1 = vu1;  // ub = u, p = 0 at the start of a warp (optflow.py:169-174)
+          vb2 = vu2;
+        } else {
+          vb1 = a.in.p[B1][o];
+          vb2 = a.in.p[B2][o];
+          q11 = a.in.p[P11][o];
+          q12 = a.in.p[P12][o];
+          q21 = a.in.p[P21][o];
+          q22 = a.in.p[P22][o];
+        }
+        vgx = a.gx[o];
+        vgy = a.gy[o];
+        vr0 = a.r0[o];
       }
-      vgx = a.gx[o];
-      vgy = a.gy[o];
-      vr0 = a.r0[o];
+      u1[q] = vu1;
+      u2[q] = vu2;
+      gx[q] = vgx;
+      gy[q] = vgy;
+      r0[q] = vr0;
+      const double g2 = vgx * vgx + vgy * vgy;  // optflow.py:163
+      const bool ok = g2 > 1e-12;
+      ig2[q] = ok ? 1.0 / (g2 > 1e-12 ? g2 : 1e-12) : 0.0;
+      thr[q] = tl * g2;  // tau*lam*grad_sq (optflow.py:176)
+      fl[q] = (gc < W - 1 ? F_R : 0u) | (gr < H - 1 ? F_D : 0u) | (gc > 0 ? F_L : 0u) |
+              (gc == W - 1 ? F_LASTC : 0u) | (gr > 0 ? F_U : 0u) | (gr == H - 1 ? F_LASTR : 0u) |
+              (ok ? F_OK : 0u);
+      const int id = base + k * BY * SP + 32 * cx;
+      sb1[id] = vb1;
+      sb2[id] = vb2;
+      sp11[id] = q11;
+      sp12[id] = q12;
+      sp21[id] = q21;
+      sp22[id] = q22;
     }
-    u1[k] = vu1;
-    u2[k] = vu2;
-    gx[k] = vgx;
-    gy[k] = vgy;
-    r0[k] = vr0;
-    const double g2 = vgx * vgx + vgy * vgy;  // optflow.py:163
-    ok[k] = g2 > 1e-12;
-    ig2[k] = ok[k] ? 1.0 / (g2 > 1e-12 ? g2 : 1e-12) : 0.0;
-    thr[k] = tl * g2;  // tau*lam*grad_sq (optflow.py:176)
-    s_b1[lr][tx] = vb1;
-    s_b2[lr][tx] = vb2;
-    s_p11[lr][tx] = q11;
-    s_p12[lr][tx] = q12;
-    s_p21[lr][tx] = q21;
-    s_p22[lr][tx] = q22;
   }
   __syncthreads();
 
-  const int txr = tx < kTW - 1 ? tx + 1 : tx;  // clamped neighbour columns
-  const int txl = tx > 0 ? tx - 1 : tx;
-  const bool has_r = gc < W - 1, has_l = gc > 0, last_c = gc == W - 1;
-
   for (int it = 0; it < a.iters; ++it) {
+    double p11[NP], p12[NP], p21[NP], p22[NP];
     // ---- dual ascent with Huber prox and unit-ball projection (:180-191)
-    double p11[kPY], p12[kPY], p21[kPY], p22[kPY];
 #pragma unroll
-    for (int k = 0; k < kPY; ++k) {
-      const int lr = ty + kBY * k, gr = oy + lr;
-      const int lrd = lr < kTH - 1 ? lr + 1 : lr;
-      const bool has_d = gr < H - 1;
-      const double c1 = s_b1[lr][tx], c2 = s_b2[lr][tx];
-      const double a1x = has_r ? s_b1[lr][txr] - c1 : 0.0;
-      const double a1y = has_d ? s_b1[lrd][tx] - c1 : 0.0;
-      const double a2x = has_r ? s_b2[lr][txr] - c2 : 0.0;
-      const double a2y = has_d ? s_b2[lrd][tx] - c2 : 0.0;
-      double q11 = (s_p11[lr][tx] + a.sigma * a1x) * a.shrink;
-      double q12 = (s_p12[lr][tx] + a.sigma * a1y) * a.shrink;
-      double q21 = (s_p21[lr][tx] + a.sigma * a2x) * a.shrink;
-      double q22 = (s_p22[lr][tx] + a.sigma * a2y) * a.shrink;
+    for (int q = 0; q < NP; ++q) {
+      const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
+      const double c1 = sb1[id], c2 = sb2[id];
+      const bool R = fl[q] & F_R, D = fl[q] & F_D;
+      const double a1x = R ? sb1[id + 1] - c1 : 0.0;
+      const double a1y = D ? sb1[id + SP] - c1 : 0.0;
+      const double a2x = R ? sb2[id + 1] - c2 : 0.0;
+      const double a2y = D ? sb2[id + SP] - c2 : 0.0;
+      double q11 = (sp11[id] + a.sigma * a1x) * a.shrink;
+      double q12 = (sp12[id] + a.sigma * a1y) * a.shrink;
+      double q21 = (sp21[id] + a.sigma * a2x) * a.shrink;
+      double q22 = (sp22[id] + a.sigma * a2y) * a.shrink;
       // n = max(1, hypot(.)); p /= n.  When |q|^2 is clearly below 1 the
       // norm is exactly 1 and the division is the identity: skip both.
       if (q11 * q11 + q12 * q12 > 0.999999) {
@@ -284,89 +319,139 @@ __global__ void __launch_bounds__(kTW *kBY, 2) k_pd_tile(const PDArgs a) {
         q21 = q21 / n2;
         q22 = q22 / n2;
       }
-      p11[k] = q11;
-      p12[k] = q12;
-      p21[k] = q21;
-      p22[k] = q22;
-    }
-    __syncthreads();  // everyone has read b and old p
-#pragma unroll
-    for (int k = 0; k < kPY; ++k) {
-      const int lr = ty + kBY * k;
-      s_p11[lr][tx] = p11[k];
-      s_p12[lr][tx] = p12[k];
-      s_p21[lr][tx] = p21[k];
-      s_p22[lr][tx] = p22[k];
+      sp11[id] = q11;  // in place: no other thread reads p in this phase
+      sp12[id] = q12;
+      sp21[id] = q21;
+      sp22[id] = q22;
+      p11[q] = q11;
+      p12[q] = q12;
+      p21[q] = q21;
+      p22[q] = q22;
     }
     __syncthreads();
     // ---- primal descent + TV-L1 shrinkage (:194-208)
 #pragma unroll
-    for (int k = 0; k < kPY; ++k) {
-      const int lr = ty + kBY * k, gr = oy + lr;
-      const int lru = lr > 0 ? lr - 1 : lr;
+    for (int q = 0; q < NP; ++q) {
+      const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
+      const unsigned f = fl[q];
       // divergence (imageops.py:41-50): dx + dy with border rules
       double dx1, dx2, dy1, dy2;
-      if (!has_l) {
-        dx1 = p11[k];
-        dx2 = p21[k];
-      } else if (last_c) {
-        dx1 = -s_p11[lr][txl];
-        dx2 = -s_p21[lr][txl];
+      if (!(f & F_L)) {
+        dx1 = p11[q];
+        dx2 = p21[q];
+      } else if (f & F_LASTC) {
+        dx1 = -sp11[id - 1];
+        dx2 = -sp21[id - 1];
       } else {
-        dx1 = p11[k] - s_p11[lr][txl];
-        dx2 = p21[k] - s_p21[lr][txl];
+        dx1 = p11[q] - sp11[id - 1];
+        dx2 = p21[q] - sp21[id - 1];
       }
-      if (gr <= 0) {
-        dy1 = p12[k];
-        dy2 = p22[k];
-      } else if (gr == H - 1) {
-        dy1 = -s_p12[lru][tx];
-        dy2 = -s_p22[lru][tx];
+      if (!(f & F_U)) {
+        dy1 = p12[q];
+        dy2 = p22[q];
+      } else if (f & F_LASTR) {
+        dy1 = -sp12[id - SP];
+        dy2 = -sp22[id - SP];
       } else {
-        dy1 = p12[k] - s_p12[lru][tx];
-        dy2 = p22[k] - s_p22[lru][tx];
+        dy1 = p12[q] - sp12[id - SP];
+        dy2 = p22[q] - sp22[id - SP];
       }
-      const double v1 = u1[k] + a.tau * (dx1 + dy1);
-      const double v2 = u2[k] + a.tau * (dx2 + dy2);
-      const double rho = r0[k] + gx[k] * v1 + gy[k] * v2;
-      const bool lo = rho < -thr[k];
-      const bool hi = rho > thr[k];
-      double d = lo ? tl : (hi ? -tl : -rho * ig2[k]);
-      d = (ok[k] || lo || hi) ? d : 0.0;
-      const double n1 = v1 + d * gx[k];
-      const double n2 = v2 + d * gy[k];
-      s_b1[lr][tx] = 2.0 * n1 - u1[k];
-      s_b2[lr][tx] = 2.0 * n2 - u2[k];
-      u1[k] = n1;
-      u2[k] = n2;
+      const double v1 = u1[q] + a.tau * (dx1 + dy1);
+      const double v2 = u2[q] + a.tau * (dx2 + dy2);
+      const double rho = r0[q] + gx[q] * v1 + gy[q] * v2;
+      const bool lo = rho < -thr[q];
+      const bool hi = rho > thr[q];
+      double d = lo ? tl : (hi ? -tl : -rho * ig2[q]);
+      d = ((f & F_OK) || lo || hi) ? d : 0.0;
+      const double n1 = v1 + d * gx[q];
+      const double n2 = v2 + d * gy[q];
+      sb1[id] = 2.0 * n1 - u1[q];  // in place: no other thread reads u-bar here
+      sb2[id] = 2.0 * n2 - u2[q];
+      u1[q] = n1;
+      u2[q] = n2;
     }
     __syncthreads();
   }
 
   // ---- write back the exact interior
-  const int lo_x = a.halo, hi_x = kTW - a.halo;
-  const int lo_y = a.halo, hi_y = kTH - a.halo;
-  if (!cin || tx < lo_x || tx >= hi_x) return;
+  const int lo_x = a.halo, hi_x = TW - a.halo;
+  const int lo_y = a.halo, hi_y = TH - a.halo;
 #pragma unroll
-  for (int k = 0; k < kPY; ++k) {
-    const int lr = ty + kBY * k, gr = oy + lr;
-    if (gr < 0 || gr >= H || lr < lo_y || lr >= hi_y) continue;
+  for (int q = 0; q < NP; ++q) {
+    const int k = q / NX, cx = q % NX;
+    const int lc = tx + 32 * cx, lr = ty + BY * k;
+    const int gc = ox + lc, gr = oy + lr;
+    if (gc < 0 || gc >= W || gr < 0 || gr >= H) continue;
+    if (lc < lo_x || lc >= hi_x || lr < lo_y || lr >= hi_y) continue;
+    const int id = base + k * BY * SP + 32 * cx;
     const int64_t o = so + (int64_t)gr * W + gc;
-    a.out.p[U1][o] = u1[k];
-    a.out.p[U2][o] = u2[k];
-    a.out.p[B1][o] = s_b1[lr][tx];
-    a.out.p[B2][o] = s_b2[lr][tx];
-    a.out.p[P11][o] = s_p11[lr][tx];
-    a.out.p[P12][o] = s_p12[lr][tx];
-    a.out.p[P21][o] = s_p21[lr][tx];
-    a.out.p[P22][o] = s_p22[lr][tx];
+    a.out.p[U1][o] = u1[q];
+    a.out.p[U2][o] = u2[q];
+    a.out.p[B1][o] = sb1[id];
+    a.out.p[B2][o] = sb2[id];
+    a.out.p[P11][o] = sp11[id];
+    a.out.p[P12][o] = sp12[id];
+    a.out.p[P21][o] = sp21[id];
+    a.out.p[P22][o] = sp22[id];
   }
 }
 
-StatePtrs state_ptrs(double *base, int nb, int64_t cap) {
-  StatePtrs s;
-  for (int k = 0; k < NST; ++k) s.p[k] = base + (int64_t)k * nb * cap;
-  return s;
+// Launch configurations (tile width x height, threads, min CTAs/SM).
+struct PDConfig {
+  int idx, tw, th, by;
+  void (*fn)(PDArgs);
+  size_t smem;
+};
+
+template <int TW, int BY, int PY, int MINB>
+PDConfig make_cfg(int idx) {
+  using G = PDGeom<TW, BY, PY>;
+  return PDConfig{idx, TW, G::TH, BY, &k_pd_tile<TW, BY, PY, MINB>, G::smem};
+}
+
+// index: 0 = 32x32/256thr, 1 = 32x32/512thr, 2 = 64x32/512thr, 3 = 64x32/256thr
+inline PDConfig pd_config(int i) {
+  switch (i) {
+    case 1: return make_cfg<32, 16, 2, 2>(1);
+    case 2: return make_cfg<64, 16, 2, 2>(2);
+    case 3: return make_cfg<64, 8, 4, 1>(3);
+    default: return make_cfg<32, 8, 4, 2>(0);
+  }
+}
+
+int pd_launch(const PDConfig &c, const PDArgs &a, int nb, cudaStream_t s) {
+  static bool attr_done[4] = {};
+  if (!attr_done[c.idx]) {
+    FT_CUDA_TRY(cudaFuncSetAttribute(c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)c.smem));
+    attr_done[c.idx] = true;
+  }
+  const int step_x = c.tw - 2 * a.halo, step_y = c.th - 2 * a.halo;
+  const dim3 grid(a.halo ? (a.w + step_x - 1) / step_x : 1, a.halo ? (a.h + step_y - 1) / step_y : 1,
+                  nb);
+  c.fn<<<grid, dim3(32, c.by), c.smem, s>>>(a);
+  count_launch();
+  return FT_OK;
+}
+
+// tile configuration + halo used for a level of w x h
+struct PDPlan {
+  PDConfig cfg;
+  int halo;
+};
+
+int env_int(const char *name, int dflt) {
+  const char *v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+
+PDPlan pd_plan(int w, int h) {
+  // coarse levels that fit one tile run resident (no halo, all iterations)
+  for (int i : {0, 2}) {
+    PDConfig c = pd_config(i);
+    if (w <= c.tw && h <= c.th) return PDPlan{c, 0};
+  }
+  return PDPlan{pd_config(env_int("FT_PD_CFG", 0)), env_int("FT_PD_HALO", 4)};
 }
 
 inline dim3 grid2d(int w, int h, int nb) { return dim3((w + 31) / 32, (h + 7) / 8, nb); }
@@ -378,10 +463,9 @@ inline dim3 grid2d(int w, int h, int nb) { return dim3((w + 31) / 32, (h + 7) / 
 // last step), bracketed by CUDA events on `s`.  Returns the mean duration.
 int profile_pd(FlowWork &fw, int w, int h, int nb, const FlowParamsD &p, int reps,
                cudaStream_t s, double *ms_per_launch, int *iters_per_launch) {
-  const int halo = (w <= kTW && h <= kTH) ? 0 : 4;
+  const PDPlan plan = pd_plan(w, h);
+  const int halo = plan.halo;
   const int iters = halo ? std::min(halo, p.iters) : p.iters;
-  const int step_x = kTW - 2 * halo, step_y = kTH - 2 * halo;
-  const dim3 pgrid(halo ? (w + step_x - 1) / step_x : 1, halo ? (h + step_y - 1) / step_y : 1, nb);
   PDArgs a;
   a.gx = fw.gx;
   a.gy = fw.gy;
@@ -405,7 +489,7 @@ int profile_pd(FlowWork &fw, int w, int h, int nb, const FlowParamsD &p, int rep
     if (r == 0) FT_CUDA_TRY(cudaEventRecord(e0, s));
     a.in = state_ptrs(fw.st[cur], fw.nb, fw.cap);
     a.out = state_ptrs(fw.st[1 - cur], fw.nb, fw.cap);
-    k_pd_tile<<<pgrid, dim3(kTW, kBY), 0, s>>>(a);
+    FT_TRY(pd_launch(plan.cfg, a, nb, s));
     cur = 1 - cur;
   }
   FT_CUDA_TRY(cudaEventRecord(e1, s));
@@ -454,7 +538,7 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
   const double sigma = 1.0 / (8.0 * p.tau);
   const double shrink = 1.0 / (1.0 + sigma * p.eps);
   const dim3 blk(32, 8);
-  const int halo_tiled = 4;
+
 
   for (int lvl = scales - 1; lvl >= 0; --lvl) {
     const int w = lw[lvl], h = lh[lvl];
@@ -479,11 +563,9 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
     k_central_grad<<<grid2d(w, h, nb), blk, 0, s>>>(i1, w, h, pyr_stride, fw.ix, fw.iy, cap);
     count_launch();
 
-    const bool resident = w <= kTW && h <= kTH;
-    const int halo = resident ? 0 : halo_tiled;
-    const int step_x = kTW - 2 * halo, step_y = kTH - 2 * halo;
-    const dim3 pgrid(resident ? 1 : (w + step_x - 1) / step_x,
-                     resident ? 1 : (h + step_y - 1) / step_y, nb);
+    const PDPlan plan = pd_plan(w, h);
+    const bool resident = plan.halo == 0;
+    const int halo = plan.halo;
     for (int wp = 0; wp < p.warps; ++wp) {
       st = state_ptrs(fw.st[cur], fw.nb, cap);
       k_warp_setup<<<grid2d(w, h, nb), blk, 0, s>>>(i0, i1, pyr_stride, fw.ix, fw.iy, st.p[U1],
@@ -508,8 +590,7 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
         a.lam = p.lam;
         a.sigma = sigma;
         a.shrink = shrink;
-        k_pd_tile<<<pgrid, dim3(kTW, kBY), 0, s>>>(a);
-        count_launch();
+        FT_TRY(pd_launch(plan.cfg, a, nb, s));
         cur = 1 - cur;
         done += n;
       }

@@ -11,72 +11,92 @@
 namespace ft {
 
 // ------------------------------------------------------------ predict
-// numpy pairwise_sum over the flattened window elements [e0, e0+n): element
-// e sits at plane[(top + e/ww)*pitch + left + e%ww].  <8: sequential; <=128:
-// eight strided accumulators folded ((0+1)+(2+3))+((4+5)+(6+7)) then the
-// tail; else split at n/2 rounded down to a multiple of 8.
+// ndarray.mean() over plane[top:bottom, left:right] exactly as numpy 2.3
+// evaluates it (verified against np.mean, tests/golden): a contiguous window
+// (one row, or the full field width) is ONE pairwise_sum run; otherwise the
+// reduction iterator buffers floor(8192/width) whole rows at a time and adds
+// each buffer's pairwise sum to a 0.0 accumulator.  pairwise_sum(n): n < 8
+// sequential; n <= 128 eight strided accumulators folded
+// ((0+1)+(2+3))+((4+5)+(6+7)) then the tail; else split at n/2 rounded down
+// to a multiple of 8 and add the halves.
+//
+// Device form: one warp per (box, component).  Lane 0 walks the pairwise
+// tree once to list its leaves (<=128 contiguous elements each), the 32 lanes
+// sum the leaves in parallel, and lane 0 walks the tree again folding the
+// leaf sums in the same post order -- same additions, same order, so the
+// result is bit-identical to numpy while the loads run 32-wide.
 struct Window {
   const double *plane;
   int64_t pitch;
   int top, left, ww;
-  __device__ __forceinline__ double at(int64_t e) const {
-    const int64_t r = e / ww;
-    return plane[(top + r) * pitch + left + (e - r * ww)];
-  }
 };
 
+// one pairwise_sum leaf over flattened elements [e0, e0+n), n <= 128
 __device__ double pw_leaf(const Window &W, int64_t e0, int64_t n) {
+  int64_t r = e0 / W.ww;
+  int c = (int)(e0 - r * W.ww);
+  const double *row = W.plane + (W.top + r) * W.pitch + W.left;
+  auto next = [&]() -> double {
+    const double v = row[c];
+    if (++c == W.ww) {
+      c = 0;
+      row += W.pitch;
+    }
+    return v;
+  };
   if (n < 8) {
     double acc = 0.0;
-    for (int64_t i = 0; i < n; ++i) acc += W.at(e0 + i);
+    for (int64_t i = 0; i < n; ++i) acc += next();
     return acc;
   }
-  double r[8];
+  double a[8];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) r[j] = W.at(e0 + j);
+  for (int j = 0; j < 8; ++j) a[j] = next();
   int64_t i = 8;
   const int64_t stop = n - (n % 8);
   for (; i < stop; i += 8) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) r[j] += W.at(e0 + i + j);
+    for (int j = 0; j < 8; ++j) a[j] += next();
   }
-  double acc = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-  for (; i < n; ++i) acc += W.at(e0 + i);
+  double acc = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+  for (; i < n; ++i) acc += next();
   return acc;
 }
 
-// iterative post-order evaluation of the pairwise tree (no device recursion)
-__device__ double pw_sum(const Window &W, int64_t e0, int64_t n) {
-  if (n <= 128) return pw_leaf(W, e0, n);
+// Post-order walk of the pairwise tree of [e0, e0+n); leaf(e, len) supplies
+// each leaf's value in order; internal nodes add left + right.
+template <typename Leaf>
+__device__ double pw_walk(int64_t e0, int64_t n, Leaf leaf) {
+  if (n <= 128) return leaf(e0, n);
   struct Node {
     int64_t e0, n;
     int state;
     double left;
   };
-  Node stack[40];
+  Node stack[48];
   int sp = 0;
   stack[0] = {e0, n, 0, 0.0};
   double ret = 0.0;
   while (true) {
     Node &t = stack[sp];
     if (t.n <= 128) {
-      ret = pw_leaf(W, t.e0, t.n);
+      ret = leaf(t.e0, t.n);
       if (sp == 0) return ret;
       --sp;
       continue;
     }
     int64_t n2 = t.n / 2;
     n2 -= n2 % 8;
-    if (t.state == 0) {  // descend left
+    if (t.state == 0) {
       t.state = 1;
       stack[sp + 1] = {t.e0, n2, 0, 0.0};
       ++sp;
-    } else if (t.state == 1) {  // left done -> descend right
+    } else if (t.state == 1) {
       t.left = ret;
       t.state = 2;
       stack[sp + 1] = {t.e0 + n2, t.n - n2, 0, 0.0};
       ++sp;
-    } else {  // both done
+    } else {
       ret = t.left + ret;
       if (sp == 0) return ret;
       --sp;
@@ -84,23 +104,63 @@ __device__ double pw_sum(const Window &W, int64_t e0, int64_t n) {
   }
 }
 
-// ndarray.mean() over plane[top:bottom, left:right] as numpy 2.3 evaluates it
-// (verified against np.mean in tests/golden): a contiguous window (one row, or
-// the full field width) is one pairwise run; otherwise the reduction iterator
-// buffers floor(8192/width) whole rows at a time and adds each buffer's
-// pairwise sum to a 0.0 accumulator.  Divided by the element count.
-__device__ double np_window_mean(const double *plane, int64_t pitch, int field_w, int top,
-                                 int bottom, int left, int right) {
+constexpr int kLeafCap = 1024;  // leaves per warp pass (n up to ~65k elements)
+struct LeafScratch {           // per-warp shared memory
+  int off[kLeafCap];
+  int len[kLeafCap];
+  double sum[kLeafCap];
+};
+
+// pairwise_sum of elements [e0, e0+n) of window W, evaluated by a full warp;
+// every lane returns the result.
+__device__ double warp_pw_sum(const Window &W, int64_t e0, int64_t n, LeafScratch &L) {
+  const int lane = threadIdx.x & 31;
+  double res = 0.0;
+  if (n <= 128) {
+    if (lane == 0) res = pw_leaf(W, e0, n);
+    return __shfl_sync(0xffffffffu, res, 0);
+  }
+  int nl = 0;
+  if (lane == 0) {
+    pw_walk(e0, n, [&](int64_t e, int64_t len) -> double {
+      if (nl < kLeafCap) {
+        L.off[nl] = (int)(e - e0);
+        L.len[nl] = (int)len;
+      }
+      ++nl;
+      return 0.0;
+    });
+  }
+  nl = __shfl_sync(0xffffffffu, nl, 0);
+  if (nl > kLeafCap) {  // enormous contiguous window: sequential walk
+    if (lane == 0) res = pw_walk(e0, n, [&](int64_t e, int64_t len) { return pw_leaf(W, e, len); });
+    return __shfl_sync(0xffffffffu, res, 0);
+  }
+  __syncwarp();
+  for (int k = lane; k < nl; k += 32) L.sum[k] = pw_leaf(W, e0 + L.off[k], L.len[k]);
+  __syncwarp();
+  if (lane == 0) {
+    int k = 0;
+    res = pw_walk(e0, n, [&](int64_t, int64_t) { return L.sum[k++]; });
+  }
+  res = __shfl_sync(0xffffffffu, res, 0);
+  __syncwarp();
+  return res;
+}
+
+__device__ double warp_window_mean(const double *plane, int64_t pitch, int field_w, int top,
+                                   int bottom, int left, int right, LeafScratch &L) {
   const int hh = bottom - top, ww = right - left;
   const int64_t n = (int64_t)hh * ww;
-  Window W{plane, pitch, top, left, ww};
+  const Window W{plane, pitch, top, left, ww};
   double total;
   if (hh == 1 || ww == field_w) {
-    total = pw_sum(W, 0, n);
+    total = warp_pw_sum(W, 0, n, L);
   } else {
     const int64_t chunk = (int64_t)(8192 / ww) * ww;
     total = 0.0;
-    for (int64_t e = 0; e < n; e += chunk) total += pw_sum(W, e, n - e < chunk ? n - e : chunk);
+    for (int64_t e = 0; e < n; e += chunk)
+      total += warp_pw_sum(W, e, n - e < chunk ? n - e : chunk, L);
   }
   return total / (double)n;
 }
@@ -111,37 +171,59 @@ __device__ __forceinline__ double rha(double v) {  // imageops.py:87-90
 __device__ __forceinline__ double py_max(double a, double b) { return b > a ? b : a; }
 __device__ __forceinline__ double py_min(double a, double b) { return b < a ? b : a; }
 
-// One box (track.py:74-86).  Returns false for "None" (empty support).
-__device__ bool predict_box(const double *box, const double *dx, const double *dy,
-                            int64_t pitch, int fw_l, int fh_l, int level, int frame_w,
-                            int frame_h, double *out) {
+// rounded, clamped pixel support of a box at pyramid `level` (track.py:74-81);
+// false when empty (predict returns None)
+__device__ __forceinline__ bool box_support(const double *box, int level, int fw_l, int fh_l,
+                                            int &top, int &bottom, int &left, int &right) {
+  const double scale = (double)(1 << level);
+  left = max((int)rha(box[0] / scale), 0);
+  top = max((int)rha(box[1] / scale), 0);
+  right = min((int)rha((box[0] + box[2]) / scale), fw_l);
+  bottom = min((int)rha((box[1] + box[3]) / scale), fh_l);
+  return right > left && bottom > top;
+}
+
+// shifted, clamped box from the two window means (track.py:82-86)
+__device__ __forceinline__ void apply_shift(const double *box, double mx, double my, int level,
+                                            int frame_w, int frame_h, double *out) {
   const double scale = (double)(1 << level);
   const double x = box[0], y = box[1], w = box[2], h = box[3];
-  const int left = max((int)rha(x / scale), 0);
-  const int top = max((int)rha(y / scale), 0);
-  const int right = min((int)rha((x + w) / scale), fw_l);
-  const int bottom = min((int)rha((y + h) / scale), fh_l);
-  if (right <= left || bottom <= top) return false;
-  const double sx = np_window_mean(dx, pitch, fw_l, top, bottom, left, right) * scale;
-  const double sy = np_window_mean(dy, pitch, fw_l, top, bottom, left, right) * scale;
+  const double sx = mx * scale, sy = my * scale;
   out[0] = py_min(py_max(x + sx, 0.0), py_max((double)frame_w - w, 0.0));
   out[1] = py_min(py_max(y + sy, 0.0), py_max((double)frame_h - h, 0.0));
   out[2] = w;
   out[3] = h;
-  return true;
 }
 
-__global__ void k_predict(const double *boxes, int n, const double *dx, const double *dy,
-                          int fw_l, int fh_l, int64_t pitch, int level, int frame_w, int frame_h,
-                          double *out, uint8_t *valid) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+constexpr int kPredWarps = 4;  // warps per predict CTA
+
+// unit predict, phase 1: one warp per (box, component) -> mean into out[4i+c]
+__global__ void __launch_bounds__(32 * kPredWarps)
+    k_predict_mean(const double *boxes, int n, const double *dx, const double *dy, int fw_l,
+                   int fh_l, int64_t pitch, int level, double *out, uint8_t *valid) {
+  extern __shared__ __align__(16) char smem[];
+  const int warp = threadIdx.x >> 5;
+  LeafScratch &L = reinterpret_cast<LeafScratch *>(smem)[warp];
+  const int item = blockIdx.x * kPredWarps + warp;
+  const int i = item >> 1, comp = item & 1;
   if (i >= n) return;
-  valid[i] = predict_box(boxes + 4 * i, dx, dy, pitch, fw_l, fh_l, level, frame_w, frame_h,
-                         out + 4 * i)
-                 ? 1
-                 : 0;
+  int top, bottom, left, right;
+  const bool ok = box_support(boxes + 4 * i, level, fw_l, fh_l, top, bottom, left, right);
+  if ((threadIdx.x & 31) == 0 && comp == 0) valid[i] = ok;
+  if (!ok) return;
+  const double m =
+      warp_window_mean(comp ? dy : dx, pitch, fw_l, top, bottom, left, right, L);
+  if ((threadIdx.x & 31) == 0) out[4 * i + comp] = m;
 }
 
+// unit predict, phase 2: means -> shifted, clamped boxes
+__global__ void k_predict_apply(const double *boxes, int n, int level, int frame_w, int frame_h,
+                                double *out, const uint8_t *valid) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || !valid[i]) return;
+  const double mx = out[4 * i], my = out[4 * i + 1];
+  apply_shift(boxes + 4 * i, mx, my, level, frame_w, frame_h, out + 4 * i);
+}
 // ------------------------------------------------------------ IoU / cost
 __device__ __forceinline__ double iou_box(const double *a, const double *b) {
   const double ix = py_max(a[0], b[0]);
@@ -361,9 +443,13 @@ int launch_predict(const double *boxes, int n, const double *dx, const double *d
                    int fh_l, int64_t pitch, int level, int frame_w, int frame_h, double *out,
                    uint8_t *valid, cudaStream_t s) {
   if (n <= 0) return FT_OK;
-  k_predict<<<(n + 63) / 64, 64, 0, s>>>(boxes, n, dx, dy, fw_l, fh_l, pitch, level, frame_w,
-                                         frame_h, out, valid);
-  count_launch();
+  const size_t sm = kPredWarps * sizeof(LeafScratch);
+  FT_CUDA_TRY(cudaFuncSetAttribute(k_predict_mean, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)sm));
+  k_predict_mean<<<(2 * n + kPredWarps - 1) / kPredWarps, 32 * kPredWarps, sm, s>>>(
+      boxes, n, dx, dy, fw_l, fh_l, pitch, level, out, valid);
+  k_predict_apply<<<(n + 127) / 128, 128, 0, s>>>(boxes, n, level, frame_w, frame_h, out, valid);
+  count_launch(2);
   FT_CUDA_TRY(cudaGetLastError());
   return FT_OK;
 }
@@ -406,23 +492,39 @@ int launch_hungarian(const double *cost, int m, int n, int has_forbidden, double
 // ============================================================ tracker step
 // One CTA per stream for every per-stream phase.
 
-// predict every active track; apply valid predictions; build the candidate
-// list (actives with a prediction, table order) -- SURVEY A16 step (4).
-__global__ void k_trk_predict(TrackerDev T, const double *dx, const double *dy,
-                              int64_t field_stride, int fw_l, int fh_l, int level) {
+// predict, phase 1: one warp per (active track, component) of every stream
+// (grid.x = stream, grid.y covers 2*cap items) -> window mean in T.pmean
+__global__ void __launch_bounds__(32 * kPredWarps)
+    k_trk_predict(TrackerDev T, const double *dx, const double *dy, int64_t field_stride, int fw_l,
+                  int fh_l, int level) {
+  extern __shared__ __align__(16) char smem[];
+  const int warp = threadIdx.x >> 5;
+  LeafScratch &L = reinterpret_cast<LeafScratch *>(smem)[warp];
+  const int s = blockIdx.x;
+  const int item = blockIdx.y * kPredWarps + warp;
+  const int i = item >> 1, comp = item & 1;
+  if (i >= T.n_active[s]) return;
+  const int64_t o = (int64_t)s * T.cap + i;
+  int top, bottom, left, right;
+  const bool ok = box_support(T.box + 4 * o, level, fw_l, fh_l, top, bottom, left, right);
+  if ((threadIdx.x & 31) == 0 && comp == 0) T.valid[o] = ok;
+  if (!ok) return;
+  const double *plane = (comp ? dy : dx) + s * field_stride;
+  const double m = warp_window_mean(plane, fw_l, fw_l, top, bottom, left, right, L);
+  if ((threadIdx.x & 31) == 0) T.pmean[2 * o + comp] = m;
+}
+
+// predict, phase 2: apply valid predictions (track.py:82-86), then build the
+// candidate list (actives with a prediction, table order) -- SURVEY A16 (4)
+__global__ void k_trk_apply(TrackerDev T, int level) {
   const int s = blockIdx.x;
   const int na = T.n_active[s];
   const int64_t tb = (int64_t)s * T.cap;
   for (int i = threadIdx.x; i < na; i += blockDim.x) {
-    double out[4];
-    const bool ok = predict_box(T.box + 4 * (tb + i), dx + s * field_stride,
-                                dy + s * field_stride, fw_l, fw_l, fh_l, level, T.frame_w,
-                                T.frame_h, out);
-    if (ok) {
-#pragma unroll
-      for (int c = 0; c < 4; ++c) T.box[4 * (tb + i) + c] = out[c];
-    }
-    T.valid[tb + i] = ok;
+    const int64_t o = tb + i;
+    if (T.valid[o])
+      apply_shift(T.box + 4 * o, T.pmean[2 * o], T.pmean[2 * o + 1], level, T.frame_w, T.frame_h,
+                  T.box + 4 * o);
   }
   __syncthreads();
   if (threadIdx.x == 0) {  // order-preserving compaction of candidates
@@ -609,8 +711,11 @@ int launch_tracker_track(TrackerDev &T, const double *dx, const double *dy, int6
                          ft_track *d_out, int32_t *d_nout, cudaStream_t s) {
   const int S = T.n_streams;
   if (has_prev) {
-    k_trk_predict<<<S, 128, 0, s>>>(T, dx, dy, fstride, fw_l, fh_l, level);
-    count_launch();
+    const dim3 pg(S, (2 * T.cap + kPredWarps - 1) / kPredWarps);
+    k_trk_predict<<<pg, 32 * kPredWarps, kPredWarps * sizeof(LeafScratch), s>>>(
+        T, dx, dy, fstride, fw_l, fh_l, level);
+    k_trk_apply<<<S, 128, 0, s>>>(T, level);
+    count_launch(2);
   } else {
     // first frame: nothing to predict, every kept detection spawns
     FT_CUDA_TRY(cudaMemsetAsync(T.n_cand, 0, S * sizeof(int32_t), s));
@@ -634,6 +739,8 @@ int tracker_kernel_setup(const TrackerDev &T) {
   if (sm > 200 * 1024) return fail(FT_EINVAL, "max_tracks/max_dets too large for one CTA");
   FT_CUDA_TRY(cudaFuncSetAttribute(k_trk_hungarian, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)sm));
+  FT_CUDA_TRY(cudaFuncSetAttribute(k_trk_predict, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(kPredWarps * sizeof(LeafScratch))));
   return FT_OK;
 }
 

@@ -213,6 +213,41 @@ def test_tracker_step_matches_reference(pkg, golden, name):
     trk.close()
 
 
+def test_tracker_level1_and_empty_detections(pkg):
+    """Frames wider than 1280 px run at pyramid level 1 (select_level, HD/UHD
+    configs C3/C4); an empty detection list on a detection frame turns every
+    active track Lost; a later frame re-spawns with fresh ids."""
+    from oracle import ftoracle as O
+    from paper_1910_06017_b200.synth import make_sequence
+    W, H, T = 1300, 200, 4
+    frames, dets = make_sequence(W, H, 6, T, seed=77, det_every=1)
+    dets[2] = []  # detector ran and found nothing
+    prm = pkg.optflow.FlowParams(warps_per_level=1, iterations_per_warp=6, pyramid_scales=3)
+    oprm = O.FlowParams(warps_per_level=1, iterations_per_warp=6, pyramid_scales=3)
+    trk = pkg.pipeline.Tracker(W, H, n_streams=1, flow_params=prm, max_tracks=64, max_dets=64)
+    st = O.StreamState()
+    for t in range(T):
+        scene = trk.step(frames[t], t, [dets[t]])[0]
+        od = None if dets[t] is None else [O.Det(d.class_id, d.label, d.score, d.box) for d in dets[t]]
+        O.step(st, frames[t], t, od, oprm)
+        assert np.array_equal(scene_rows(scene), scene_rows(st.tracks)), t
+    assert any(o.state == "lost" and o.lost_at == 2 for o in scene)
+    dx, _ = trk.field(0)
+    assert dx.shape == (H // 2, W // 2)
+    trk.close()
+
+
+def test_tracker_capacity_error(pkg):
+    from paper_1910_06017_b200.detect import Detection
+    trk = pkg.pipeline.Tracker(64, 48, n_streams=1, max_tracks=2, max_dets=8)
+    dets = [Detection(0, "a", 0.9, (float(4 * i), 2.0, 3.0, 3.0)) for i in range(5)]
+    with pytest.raises(Exception, match="max_tracks"):
+        trk.step(np.zeros((48, 64), np.uint8), 0, [dets])
+    with pytest.raises(ValueError):
+        trk.step(np.zeros((48, 64), np.uint8), 1, [dets * 2])  # > max_dets
+    trk.close()
+
+
 def test_tracker_multistream_matches_oracle(pkg):
     """Several independent streams in one lockstep tracker: each stream's
     output equals the oracle run on that stream alone (stream isolation)."""

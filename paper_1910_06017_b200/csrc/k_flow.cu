@@ -396,12 +396,184 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const PDArgs a) {
   }
 }
 
+// ------------------------------------------------------------------------
+// Register-strip variant.  Tile = 32 columns x (BY*PY) rows; lane = column,
+// warp w owns rows [w*PY, w*PY+PY) as a vertical strip held entirely in
+// registers (u, u-bar, p, gathered gradient, rho0, threshold, 1/|grad|^2).
+// x-neighbours come from warp shuffles (u-bar at x+1 in the dual step, p at
+// x-1 in the primal step); y-neighbours are in the same thread except at the
+// strip ends, where one row per warp is exchanged through shared memory
+// (each warp publishes its first-row u-bar for the warp above and its
+// last-row p for the warp below).  Lanes / warps at the tile edge read their
+// own values instead of a neighbour's: those pixels are halo (or image
+// border, where the reference does not read the neighbour), exactly as in
+// k_pd_tile.  Same arithmetic, same operation order, bit-identical results.
+// ------------------------------------------------------------------------
+template <int BY, int PY, int MINB>
+__global__ void __launch_bounds__(32 * BY, MINB) k_pd_strip(const PDArgs a) {
+  constexpr int TH = BY * PY;
+  __shared__ double s_b1[BY][32], s_b2[BY][32];    // first-row u-bar of each warp
+  __shared__ double s_p12[BY][32], s_p22[BY][32];  // last-row p of each warp
+  const int W = a.w, H = a.h;
+  const int step_x = 32 - 2 * a.halo, step_y = TH - 2 * a.halo;
+  const int ox = blockIdx.x * step_x - a.halo;
+  const int oy = blockIdx.y * step_y - a.halo;
+  const int64_t so = blockIdx.z * a.cap;
+  const int lane = threadIdx.x, w = threadIdx.y;
+  const int gc = ox + lane;
+  const int gr0 = oy + w * PY;
+  const bool cin = gc >= 0 && gc < W;
+  const bool fR = gc < W - 1, fL = gc > 0, fLastC = gc == W - 1;
+  const int wd = w < BY - 1 ? w + 1 : w;  // warp below / above (self at tile edge)
+  const int wu = w > 0 ? w - 1 : w;
+
+  const double tl = a.tau * a.lam;
+  double u1[PY], u2[PY], b1[PY], b2[PY], p11[PY], p12[PY], p21[PY], p22[PY];
+  double gx[PY], gy[PY], r0[PY], thr[PY], ig2[PY];
+#pragma unroll
+  for (int k = 0; k < PY; ++k) {
+    const int gr = gr0 + k;
+    const bool in = cin && gr >= 0 && gr < H;
+    const int64_t o = so + (int64_t)gr * W + gc;
+    double vu1 = 0, vu2 = 0, vb1 = 0, vb2 = 0, q11 = 0, q12 = 0, q21 = 0, q22 = 0;
+    double vgx = 0, vgy = 0, vr0 = 0;
+    if (in) {
+      vu1 = a.in.p[U1][o];
+      vu2 = a.in.p[U2][o];
+      if (a.first) {
+        vb1 = vu1;  // ub = u, p = 0 at the start of a warp (optflow.py:169-174)
+        vb2 = vu2;
+      } else {
+        vb1 = a.in.p[B1][o];
+        vb2 = a.in.p[B2][o];
+        q11 = a.in.p[P11][o];
+        q12 = a.in.p[P12][o];
+        q21 = a.in.p[P21][o];
+        q22 = a.in.p[P22][o];
+      }
+      vgx = a.gx[o];
+      vgy = a.gy[o];
+      vr0 = a.r0[o];
+    }
+    u1[k] = vu1;
+    u2[k] = vu2;
+    b1[k] = vb1;
+    b2[k] = vb2;
+    p11[k] = q11;
+    p12[k] = q12;
+    p21[k] = q21;
+    p22[k] = q22;
+    gx[k] = vgx;
+    gy[k] = vgy;
+    r0[k] = vr0;
+    const double g2 = vgx * vgx + vgy * vgy;  // optflow.py:163
+    ig2[k] = g2 > 1e-12 ? 1.0 / g2 : 0.0;     // == 1/max(g2,1e-12) where safe
+    thr[k] = tl * g2;                          // optflow.py:176
+  }
+  s_b1[w][lane] = b1[0];
+  s_b2[w][lane] = b2[0];
+  __syncthreads();
+
+  for (int it = 0; it < a.iters; ++it) {
+    // ---- dual ascent with Huber prox and unit-ball projection (:180-191)
+    const double db1 = s_b1[wd][lane], db2 = s_b2[wd][lane];  // row below the strip
+#pragma unroll
+    for (int k = 0; k < PY; ++k) {
+      const int gr = gr0 + k;
+      const double r1 = __shfl_down_sync(0xffffffffu, b1[k], 1);
+      const double r2 = __shfl_down_sync(0xffffffffu, b2[k], 1);
+      const double d1 = k < PY - 1 ? b1[k + 1] : db1;
+      const double d2 = k < PY - 1 ? b2[k + 1] : db2;
+      const bool fD = gr < H - 1;
+      const double a1x = fR ? r1 - b1[k] : 0.0;
+      const double a1y = fD ? d1 - b1[k] : 0.0;
+      const double a2x = fR ? r2 - b2[k] : 0.0;
+      const double a2y = fD ? d2 - b2[k] : 0.0;
+      double q11 = (p11[k] + a.sigma * a1x) * a.shrink;
+      double q12 = (p12[k] + a.sigma * a1y) * a.shrink;
+      double q21 = (p21[k] + a.sigma * a2x) * a.shrink;
+      double q22 = (p22[k] + a.sigma * a2y) * a.shrink;
+      if (q11 * q11 + q12 * q12 > 0.999999) {
+        const double n1 = np_max(1.0, glibc_hypot(q11, q12));
+        q11 = q11 / n1;
+        q12 = q12 / n1;
+      }
+      if (q21 * q21 + q22 * q22 > 0.999999) {
+        const double n2 = np_max(1.0, glibc_hypot(q21, q22));
+        q21 = q21 / n2;
+        q22 = q22 / n2;
+      }
+      p11[k] = q11;
+      p12[k] = q12;
+      p21[k] = q21;
+      p22[k] = q22;
+    }
+    s_p12[w][lane] = p12[PY - 1];
+    s_p22[w][lane] = p22[PY - 1];
+    __syncthreads();
+    // ---- primal descent + TV-L1 shrinkage (:194-208)
+    const double up12 = s_p12[wu][lane], up22 = s_p22[wu][lane];  // row above the strip
+#pragma unroll
+    for (int k = 0; k < PY; ++k) {
+      const int gr = gr0 + k;
+      const double l11 = __shfl_up_sync(0xffffffffu, p11[k], 1);
+      const double l21 = __shfl_up_sync(0xffffffffu, p21[k], 1);
+      const double a12 = k > 0 ? p12[k - 1] : up12;
+      const double a22 = k > 0 ? p22[k - 1] : up22;
+      // divergence (imageops.py:41-50): dx + dy with border rules
+      const double dx1 = !fL ? p11[k] : (fLastC ? -l11 : p11[k] - l11);
+      const double dx2 = !fL ? p21[k] : (fLastC ? -l21 : p21[k] - l21);
+      const double dy1 = gr <= 0 ? p12[k] : (gr == H - 1 ? -a12 : p12[k] - a12);
+      const double dy2 = gr <= 0 ? p22[k] : (gr == H - 1 ? -a22 : p22[k] - a22);
+      const double v1 = u1[k] + a.tau * (dx1 + dy1);
+      const double v2 = u2[k] + a.tau * (dx2 + dy2);
+      const double rho = r0[k] + gx[k] * v1 + gy[k] * v2;
+      const bool lo = rho < -thr[k];
+      const bool hi = rho > thr[k];
+      double d = lo ? tl : (hi ? -tl : -rho * ig2[k]);
+      // ig2 == 0 exactly when |grad|^2 <= 1e-12 (the reference's ~safe)
+      d = (ig2[k] != 0.0 || lo || hi) ? d : 0.0;
+      const double n1 = v1 + d * gx[k];
+      const double n2 = v2 + d * gy[k];
+      b1[k] = 2.0 * n1 - u1[k];
+      b2[k] = 2.0 * n2 - u2[k];
+      u1[k] = n1;
+      u2[k] = n2;
+    }
+    s_b1[w][lane] = b1[0];
+    s_b2[w][lane] = b2[0];
+    __syncthreads();
+  }
+
+  // ---- write back the exact interior
+  if (!cin || lane < a.halo || lane >= 32 - a.halo) return;
+#pragma unroll
+  for (int k = 0; k < PY; ++k) {
+    const int lr = w * PY + k, gr = gr0 + k;
+    if (gr < 0 || gr >= H || lr < a.halo || lr >= TH - a.halo) continue;
+    const int64_t o = so + (int64_t)gr * W + gc;
+    a.out.p[U1][o] = u1[k];
+    a.out.p[U2][o] = u2[k];
+    a.out.p[B1][o] = b1[k];
+    a.out.p[B2][o] = b2[k];
+    a.out.p[P11][o] = p11[k];
+    a.out.p[P12][o] = p12[k];
+    a.out.p[P21][o] = p21[k];
+    a.out.p[P22][o] = p22[k];
+  }
+}
+
 // Launch configurations (tile width x height, threads, min CTAs/SM).
 struct PDConfig {
   int idx, tw, th, by;
   void (*fn)(PDArgs);
   size_t smem;
 };
+
+template <int BY, int PY, int MINB>
+PDConfig make_strip_cfg(int idx) {
+  return PDConfig{idx, 32, BY * PY, BY, &k_pd_strip<BY, PY, MINB>, 0};
+}
 
 template <int TW, int BY, int PY, int MINB>
 PDConfig make_cfg(int idx) {
@@ -415,12 +587,19 @@ inline PDConfig pd_config(int i) {
     case 1: return make_cfg<32, 16, 2, 2>(1);
     case 2: return make_cfg<64, 16, 2, 2>(2);
     case 3: return make_cfg<64, 8, 4, 1>(3);
+    // register strips: 32 x (BY*PY) tiles
+    case 4: return make_strip_cfg<8, 4, 1>(4);
+    case 5: return make_strip_cfg<8, 3, 2>(5);
+    case 6: return make_strip_cfg<16, 3, 1>(6);
+    case 7: return make_strip_cfg<16, 2, 1>(7);
+    case 8: return make_strip_cfg<8, 2, 2>(8);
+    case 9: return make_strip_cfg<16, 4, 1>(9);
     default: return make_cfg<32, 8, 4, 2>(0);
   }
 }
 
 int pd_launch(const PDConfig &c, const PDArgs &a, int nb, cudaStream_t s) {
-  static bool attr_done[4] = {};
+  static bool attr_done[16] = {};
   if (!attr_done[c.idx]) {
     FT_CUDA_TRY(cudaFuncSetAttribute(c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)c.smem));
@@ -451,7 +630,9 @@ PDPlan pd_plan(int w, int h) {
     PDConfig c = pd_config(i);
     if (w <= c.tw && h <= c.th) return PDPlan{c, 0};
   }
-  return PDPlan{pd_config(env_int("FT_PD_CFG", 0)), env_int("FT_PD_HALO", 4)};
+  // defaults from the sweep on B200 (profiles/README.md): 32x32 tile,
+  // 512 threads, halo 3
+  return PDPlan{pd_config(env_int("FT_PD_CFG", 1)), env_int("FT_PD_HALO", 3)};
 }
 
 inline dim3 grid2d(int w, int h, int nb) { return dim3((w + 31) / 32, (h + 7) / 8, nb); }

@@ -205,7 +205,8 @@ template <int TW, int BY, int PY>
 struct PDGeom {
   static constexpr int NX = TW / 32, TH = BY * PY, NP = NX * PY;
   static constexpr int SP = TW + 2, SR = TH + 2, PLANE = SP * SR;
-  static constexpr size_t smem = 6 * PLANE * sizeof(double);
+  // 6 exchange planes + per-warp projection queue (2*NP pairs per lane)
+  static constexpr size_t smem = 6 * PLANE * sizeof(double) + BY * 2 * NP * 32 * 16;
 };
 
 template <int TW, int BY, int PY, int MINB>
@@ -291,42 +292,83 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const PDArgs a) {
   }
   __syncthreads();
 
+  double2 *const queue = reinterpret_cast<double2 *>(sm + 6 * PL) + ty * (2 * NP * 32);
+  const unsigned lt_mask = (1u << tx) - 1u;
+
   for (int it = 0; it < a.iters; ++it) {
     double p11[NP], p12[NP], p21[NP], p22[NP];
-    // ---- dual ascent with Huber prox and unit-ball projection (:180-191)
+    // ---- dual ascent with Huber prox (:180-185); the apron makes the
+    // neighbour loads safe, the border flags select the reference's zeros
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
       const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
       const double c1 = sb1[id], c2 = sb2[id];
+      const double r1 = sb1[id + 1], r2 = sb2[id + 1], d1 = sb1[id + SP], d2 = sb2[id + SP];
       const bool R = fl[q] & F_R, D = fl[q] & F_D;
-      const double a1x = R ? sb1[id + 1] - c1 : 0.0;
-      const double a1y = D ? sb1[id + SP] - c1 : 0.0;
-      const double a2x = R ? sb2[id + 1] - c2 : 0.0;
-      const double a2y = D ? sb2[id + SP] - c2 : 0.0;
-      double q11 = (sp11[id] + a.sigma * a1x) * a.shrink;
-      double q12 = (sp12[id] + a.sigma * a1y) * a.shrink;
-      double q21 = (sp21[id] + a.sigma * a2x) * a.shrink;
-      double q22 = (sp22[id] + a.sigma * a2y) * a.shrink;
-      // n = max(1, hypot(.)); p /= n.  When |q|^2 is clearly below 1 the
-      // norm is exactly 1 and the division is the identity: skip both.
-      if (q11 * q11 + q12 * q12 > 0.999999) {
-        const double n1 = np_max(1.0, glibc_hypot(q11, q12));
-        q11 = q11 / n1;
-        q12 = q12 / n1;
+      const double a1x = R ? r1 - c1 : 0.0;
+      const double a1y = D ? d1 - c1 : 0.0;
+      const double a2x = R ? r2 - c2 : 0.0;
+      const double a2y = D ? d2 - c2 : 0.0;
+      p11[q] = (sp11[id] + a.sigma * a1x) * a.shrink;
+      p12[q] = (sp12[id] + a.sigma * a1y) * a.shrink;
+      p21[q] = (sp21[id] + a.sigma * a2x) * a.shrink;
+      p22[q] = (sp22[id] + a.sigma * a2y) * a.shrink;
+    }
+    // ---- unit-ball projection n = max(1, hypot(.)); p /= n (:186-191).
+    // When |q|^2 is clearly below 1 the norm is exactly 1 and p/1 == p, so
+    // only the few saturated pairs need hypot + two divisions.  They are
+    // compacted into a per-warp queue (ballot + popc) and processed by all
+    // 32 lanes together, instead of up to 2*NP divergent passes per warp.
+    {
+      unsigned need = 0;
+#pragma unroll
+      for (int q = 0; q < NP; ++q) {
+        if (p11[q] * p11[q] + p12[q] * p12[q] > 0.999999) need |= 1u << (2 * q);
+        if (p21[q] * p21[q] + p22[q] * p22[q] > 0.999999) need |= 1u << (2 * q + 1);
       }
-      if (q21 * q21 + q22 * q22 > 0.999999) {
-        const double n2 = np_max(1.0, glibc_hypot(q21, q22));
-        q21 = q21 / n2;
-        q22 = q22 / n2;
+      int off[2 * NP];
+      int total = 0;
+#pragma unroll
+      for (int j = 0; j < 2 * NP; ++j) {
+        const unsigned m = __ballot_sync(0xffffffffu, (need >> j) & 1u);
+        off[j] = total + __popc(m & lt_mask);
+        total += __popc(m);
       }
-      sp11[id] = q11;  // in place: no other thread reads p in this phase
-      sp12[id] = q12;
-      sp21[id] = q21;
-      sp22[id] = q22;
-      p11[q] = q11;
-      p12[q] = q12;
-      p21[q] = q21;
-      p22[q] = q22;
+      if (total) {  // warp-uniform
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+          if (need & (1u << (2 * q))) queue[off[2 * q]] = make_double2(p11[q], p12[q]);
+          if (need & (1u << (2 * q + 1))) queue[off[2 * q + 1]] = make_double2(p21[q], p22[q]);
+        }
+        __syncwarp();
+        for (int t = tx; t < total; t += 32) {
+          const double2 v = queue[t];
+          const double n = np_max(1.0, glibc_hypot(v.x, v.y));
+          queue[t] = make_double2(v.x / n, v.y / n);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+          if (need & (1u << (2 * q))) {
+            const double2 v = queue[off[2 * q]];
+            p11[q] = v.x;
+            p12[q] = v.y;
+          }
+          if (need & (1u << (2 * q + 1))) {
+            const double2 v = queue[off[2 * q + 1]];
+            p21[q] = v.x;
+            p22[q] = v.y;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
+      sp11[id] = p11[q];  // in place: no other thread reads p in this phase
+      sp12[id] = p12[q];
+      sp21[id] = p21[q];
+      sp22[id] = p22[q];
     }
     __syncthreads();
     // ---- primal descent + TV-L1 shrinkage (:194-208)
@@ -335,27 +377,13 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const PDArgs a) {
       const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
       const unsigned f = fl[q];
       // divergence (imageops.py:41-50): dx + dy with border rules
-      double dx1, dx2, dy1, dy2;
-      if (!(f & F_L)) {
-        dx1 = p11[q];
-        dx2 = p21[q];
-      } else if (f & F_LASTC) {
-        dx1 = -sp11[id - 1];
-        dx2 = -sp21[id - 1];
-      } else {
-        dx1 = p11[q] - sp11[id - 1];
-        dx2 = p21[q] - sp21[id - 1];
-      }
-      if (!(f & F_U)) {
-        dy1 = p12[q];
-        dy2 = p22[q];
-      } else if (f & F_LASTR) {
-        dy1 = -sp12[id - SP];
-        dy2 = -sp22[id - SP];
-      } else {
-        dy1 = p12[q] - sp12[id - SP];
-        dy2 = p22[q] - sp22[id - SP];
-      }
+      const double l11 = sp11[id - 1], l21 = sp21[id - 1];
+      const double u12 = sp12[id - SP], u22 = sp22[id - SP];
+      const bool L = f & F_L, LC = f & F_LASTC, U = f & F_U, LR = f & F_LASTR;
+      const double dx1 = L ? (LC ? -l11 : p11[q] - l11) : p11[q];
+      const double dx2 = L ? (LC ? -l21 : p21[q] - l21) : p21[q];
+      const double dy1 = U ? (LR ? -u12 : p12[q] - u12) : p12[q];
+      const double dy2 = U ? (LR ? -u22 : p22[q] - u22) : p22[q];
       const double v1 = u1[q] + a.tau * (dx1 + dy1);
       const double v2 = u2[q] + a.tau * (dx2 + dy2);
       const double rho = r0[q] + gx[q] * v1 + gy[q] * v2;
@@ -594,6 +622,8 @@ inline PDConfig pd_config(int i) {
     case 7: return make_strip_cfg<16, 2, 1>(7);
     case 8: return make_strip_cfg<8, 2, 2>(8);
     case 9: return make_strip_cfg<16, 4, 1>(9);
+    case 10: return make_cfg<32, 16, 2, 1>(10);
+    case 11: return make_cfg<32, 32, 1, 1>(11);
     default: return make_cfg<32, 8, 4, 2>(0);
   }
 }

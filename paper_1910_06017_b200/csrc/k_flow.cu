@@ -15,9 +15,13 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "ft_internal.cuh"
 
 namespace ft {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -199,7 +203,7 @@ struct PDArgs {
 };
 
 // per-pixel border flags (global position, fixed for the launch)
-enum : unsigned { F_R = 1, F_D = 2, F_L = 4, F_LASTC = 8, F_U = 16, F_LASTR = 32, F_OK = 64 };
+enum : unsigned { FL_R = 1, FL_D = 2, FL_L = 4, FL_LASTC = 8, FL_U = 16, FL_LASTR = 32, FL_OK = 64 };
 
 template <int TW, int BY, int PY>
 struct PDGeom {
@@ -208,6 +212,135 @@ struct PDGeom {
   // 6 exchange planes + per-warp projection queue (2*NP pairs per lane)
   static constexpr size_t smem = 6 * PLANE * sizeof(double) + BY * 2 * NP * 32 * 16;
 };
+
+// `iters` primal-dual iterations over a tile held in shared memory (the six
+// exchange planes with apron) and registers (pointwise fields); `xch` runs
+// after each half step's shared-memory writes (a block barrier in the tiled
+// kernel, the DSMEM edge exchange in the cluster kernel).
+template <int TW, int BY, int PY, typename X>
+__device__ __forceinline__ void pd_iterate(int iters, double *sm, int base, int tx,
+                                           const unsigned *fl, double *u1, double *u2,
+                                           const double *gx, const double *gy, const double *r0,
+                                           const double *thr, const double *ig2, double tau,
+                                           double tl, double sigma, double shrink, double2 *queue,
+                                           X &xch) {
+  using G = PDGeom<TW, BY, PY>;
+  constexpr int NX = G::NX, NP = G::NP, SP = G::SP, PL = G::PLANE;
+  double *const sb1 = sm, *const sb2 = sm + PL, *const sp11 = sm + 2 * PL;
+  double *const sp12 = sm + 3 * PL, *const sp21 = sm + 4 * PL, *const sp22 = sm + 5 * PL;
+  const unsigned lt_mask = (1u << tx) - 1u;
+  for (int it = 0; it < iters; ++it) {
+    double p11[NP], p12[NP], p21[NP], p22[NP];
+    // ---- dual ascent with Huber prox (:180-185); the apron makes the
+    // neighbour loads safe, the border flags select the reference's zeros
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
+      const double c1 = sb1[id], c2 = sb2[id];
+      const double r1 = sb1[id + 1], r2 = sb2[id + 1], d1 = sb1[id + SP], d2 = sb2[id + SP];
+      const bool R = fl[q] & FL_R, D = fl[q] & FL_D;
+      const double a1x = R ? r1 - c1 : 0.0;
+      const double a1y = D ? d1 - c1 : 0.0;
+      const double a2x = R ? r2 - c2 : 0.0;
+      const double a2y = D ? d2 - c2 : 0.0;
+      p11[q] = (sp11[id] + sigma * a1x) * shrink;
+      p12[q] = (sp12[id] + sigma * a1y) * shrink;
+      p21[q] = (sp21[id] + sigma * a2x) * shrink;
+      p22[q] = (sp22[id] + sigma * a2y) * shrink;
+    }
+    // ---- unit-ball projection n = max(1, hypot(.)); p /= n (:186-191).
+    // When |q|^2 is clearly below 1 the norm is exactly 1 and p/1 == p, so
+    // only the few saturated pairs need hypot + two divisions.  They are
+    // compacted into a per-warp queue (ballot + popc) and processed by all
+    // 32 lanes together, instead of up to 2*NP divergent passes per warp.
+    {
+      unsigned need = 0;
+#pragma unroll
+      for (int q = 0; q < NP; ++q) {
+        if (p11[q] * p11[q] + p12[q] * p12[q] > 0.999999) need |= 1u << (2 * q);
+        if (p21[q] * p21[q] + p22[q] * p22[q] > 0.999999) need |= 1u << (2 * q + 1);
+      }
+      int off[2 * NP];
+      int total = 0;
+#pragma unroll
+      for (int j = 0; j < 2 * NP; ++j) {
+        const unsigned m = __ballot_sync(0xffffffffu, (need >> j) & 1u);
+        off[j] = total + __popc(m & lt_mask);
+        total += __popc(m);
+      }
+      if (total) {  // warp-uniform
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+          if (need & (1u << (2 * q))) queue[off[2 * q]] = make_double2(p11[q], p12[q]);
+          if (need & (1u << (2 * q + 1))) queue[off[2 * q + 1]] = make_double2(p21[q], p22[q]);
+        }
+        __syncwarp();
+        for (int t = tx; t < total; t += 32) {
+          const double2 v = queue[t];
+          const double n = np_max(1.0, glibc_hypot(v.x, v.y));
+          queue[t] = make_double2(v.x / n, v.y / n);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+          if (need & (1u << (2 * q))) {
+            const double2 v = queue[off[2 * q]];
+            p11[q] = v.x;
+            p12[q] = v.y;
+          }
+          if (need & (1u << (2 * q + 1))) {
+            const double2 v = queue[off[2 * q + 1]];
+            p21[q] = v.x;
+            p22[q] = v.y;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
+      sp11[id] = p11[q];  // in place: no other thread reads p in this phase
+      sp12[id] = p12[q];
+      sp21[id] = p21[q];
+      sp22[id] = p22[q];
+    }
+    xch.after_dual();
+    // ---- primal descent + TV-L1 shrinkage (:194-208)
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
+      const unsigned f = fl[q];
+      // divergence (imageops.py:41-50): dx + dy with border rules
+      const double l11 = sp11[id - 1], l21 = sp21[id - 1];
+      const double u12 = sp12[id - SP], u22 = sp22[id - SP];
+      const bool L = f & FL_L, LC = f & FL_LASTC, U = f & FL_U, LR = f & FL_LASTR;
+      const double dx1 = L ? (LC ? -l11 : p11[q] - l11) : p11[q];
+      const double dx2 = L ? (LC ? -l21 : p21[q] - l21) : p21[q];
+      const double dy1 = U ? (LR ? -u12 : p12[q] - u12) : p12[q];
+      const double dy2 = U ? (LR ? -u22 : p22[q] - u22) : p22[q];
+      const double v1 = u1[q] + tau * (dx1 + dy1);
+      const double v2 = u2[q] + tau * (dx2 + dy2);
+      const double rho = r0[q] + gx[q] * v1 + gy[q] * v2;
+      const bool lo = rho < -thr[q];
+      const bool hi = rho > thr[q];
+      double d = lo ? tl : (hi ? -tl : -rho * ig2[q]);
+      d = ((f & FL_OK) || lo || hi) ? d : 0.0;
+      const double n1 = v1 + d * gx[q];
+      const double n2 = v2 + d * gy[q];
+      sb1[id] = 2.0 * n1 - u1[q];  // in place: no other thread reads u-bar here
+      sb2[id] = 2.0 * n2 - u2[q];
+      u1[q] = n1;
+      u2[q] = n2;
+    }
+    xch.after_primal();
+  }
+}
+
+struct BlockBarrier {
+  __device__ __forceinline__ void after_dual() { __syncthreads(); }
+  __device__ __forceinline__ void after_primal() { __syncthreads(); }
+};
+
 
 template <int TW, int BY, int PY, int MINB>
 __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const PDArgs a) {
@@ -278,9 +411,9 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const PDArgs a) {
       const bool ok = g2 > 1e-12;
       ig2[q] = ok ? 1.0 / (g2 > 1e-12 ? g2 : 1e-12) : 0.0;
       thr[q] = tl * g2;  // tau*lam*grad_sq (optflow.py:176)
-      fl[q] = (gc < W - 1 ? F_R : 0u) | (gr < H - 1 ? F_D : 0u) | (gc > 0 ? F_L : 0u) |
-              (gc == W - 1 ? F_LASTC : 0u) | (gr > 0 ? F_U : 0u) | (gr == H - 1 ? F_LASTR : 0u) |
-              (ok ? F_OK : 0u);
+      fl[q] = (gc < W - 1 ? FL_R : 0u) | (gr < H - 1 ? FL_D : 0u) | (gc > 0 ? FL_L : 0u) |
+              (gc == W - 1 ? FL_LASTC : 0u) | (gr > 0 ? FL_U : 0u) | (gr == H - 1 ? FL_LASTR : 0u) |
+              (ok ? FL_OK : 0u);
       const int id = base + k * BY * SP + 32 * cx;
       sb1[id] = vb1;
       sb2[id] = vb2;
@@ -293,113 +426,9 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const PDArgs a) {
   __syncthreads();
 
   double2 *const queue = reinterpret_cast<double2 *>(sm + 6 * PL) + ty * (2 * NP * 32);
-  const unsigned lt_mask = (1u << tx) - 1u;
-
-  for (int it = 0; it < a.iters; ++it) {
-    double p11[NP], p12[NP], p21[NP], p22[NP];
-    // ---- dual ascent with Huber prox (:180-185); the apron makes the
-    // neighbour loads safe, the border flags select the reference's zeros
-#pragma unroll
-    for (int q = 0; q < NP; ++q) {
-      const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
-      const double c1 = sb1[id], c2 = sb2[id];
-      const double r1 = sb1[id + 1], r2 = sb2[id + 1], d1 = sb1[id + SP], d2 = sb2[id + SP];
-      const bool R = fl[q] & F_R, D = fl[q] & F_D;
-      const double a1x = R ? r1 - c1 : 0.0;
-      const double a1y = D ? d1 - c1 : 0.0;
-      const double a2x = R ? r2 - c2 : 0.0;
-      const double a2y = D ? d2 - c2 : 0.0;
-      p11[q] = (sp11[id] + a.sigma * a1x) * a.shrink;
-      p12[q] = (sp12[id] + a.sigma * a1y) * a.shrink;
-      p21[q] = (sp21[id] + a.sigma * a2x) * a.shrink;
-      p22[q] = (sp22[id] + a.sigma * a2y) * a.shrink;
-    }
-    // ---- unit-ball projection n = max(1, hypot(.)); p /= n (:186-191).
-    // When |q|^2 is clearly below 1 the norm is exactly 1 and p/1 == p, so
-    // only the few saturated pairs need hypot + two divisions.  They are
-    // compacted into a per-warp queue (ballot + popc) and processed by all
-    // 32 lanes together, instead of up to 2*NP divergent passes per warp.
-    {
-      unsigned need = 0;
-#pragma unroll
-      for (int q = 0; q < NP; ++q) {
-        if (p11[q] * p11[q] + p12[q] * p12[q] > 0.999999) need |= 1u << (2 * q);
-        if (p21[q] * p21[q] + p22[q] * p22[q] > 0.999999) need |= 1u << (2 * q + 1);
-      }
-      int off[2 * NP];
-      int total = 0;
-#pragma unroll
-      for (int j = 0; j < 2 * NP; ++j) {
-        const unsigned m = __ballot_sync(0xffffffffu, (need >> j) & 1u);
-        off[j] = total + __popc(m & lt_mask);
-        total += __popc(m);
-      }
-      if (total) {  // warp-uniform
-#pragma unroll
-        for (int q = 0; q < NP; ++q) {
-          if (need & (1u << (2 * q))) queue[off[2 * q]] = make_double2(p11[q], p12[q]);
-          if (need & (1u << (2 * q + 1))) queue[off[2 * q + 1]] = make_double2(p21[q], p22[q]);
-        }
-        __syncwarp();
-        for (int t = tx; t < total; t += 32) {
-          const double2 v = queue[t];
-          const double n = np_max(1.0, glibc_hypot(v.x, v.y));
-          queue[t] = make_double2(v.x / n, v.y / n);
-        }
-        __syncwarp();
-#pragma unroll
-        for (int q = 0; q < NP; ++q) {
-          if (need & (1u << (2 * q))) {
-            const double2 v = queue[off[2 * q]];
-            p11[q] = v.x;
-            p12[q] = v.y;
-          }
-          if (need & (1u << (2 * q + 1))) {
-            const double2 v = queue[off[2 * q + 1]];
-            p21[q] = v.x;
-            p22[q] = v.y;
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < NP; ++q) {
-      const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
-      sp11[id] = p11[q];  // in place: no other thread reads p in this phase
-      sp12[id] = p12[q];
-      sp21[id] = p21[q];
-      sp22[id] = p22[q];
-    }
-    __syncthreads();
-    // ---- primal descent + TV-L1 shrinkage (:194-208)
-#pragma unroll
-    for (int q = 0; q < NP; ++q) {
-      const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
-      const unsigned f = fl[q];
-      // divergence (imageops.py:41-50): dx + dy with border rules
-      const double l11 = sp11[id - 1], l21 = sp21[id - 1];
-      const double u12 = sp12[id - SP], u22 = sp22[id - SP];
-      const bool L = f & F_L, LC = f & F_LASTC, U = f & F_U, LR = f & F_LASTR;
-      const double dx1 = L ? (LC ? -l11 : p11[q] - l11) : p11[q];
-      const double dx2 = L ? (LC ? -l21 : p21[q] - l21) : p21[q];
-      const double dy1 = U ? (LR ? -u12 : p12[q] - u12) : p12[q];
-      const double dy2 = U ? (LR ? -u22 : p22[q] - u22) : p22[q];
-      const double v1 = u1[q] + a.tau * (dx1 + dy1);
-      const double v2 = u2[q] + a.tau * (dx2 + dy2);
-      const double rho = r0[q] + gx[q] * v1 + gy[q] * v2;
-      const bool lo = rho < -thr[q];
-      const bool hi = rho > thr[q];
-      double d = lo ? tl : (hi ? -tl : -rho * ig2[q]);
-      d = ((f & F_OK) || lo || hi) ? d : 0.0;
-      const double n1 = v1 + d * gx[q];
-      const double n2 = v2 + d * gy[q];
-      sb1[id] = 2.0 * n1 - u1[q];  // in place: no other thread reads u-bar here
-      sb2[id] = 2.0 * n2 - u2[q];
-      u1[q] = n1;
-      u2[q] = n2;
-    }
-    __syncthreads();
-  }
+  BlockBarrier bar;
+  pd_iterate<TW, BY, PY>(a.iters, sm, base, tx, fl, u1, u2, gx, gy, r0, thr, ig2, a.tau, tl,
+                         a.sigma, a.shrink, queue, bar);
 
   // ---- write back the exact interior
   const int lo_x = a.halo, hi_x = TW - a.halo;
@@ -591,6 +620,203 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_strip(const PDArgs a) {
   }
 }
 
+// ------------------------------------------------------------------------
+// Cluster-resident coarse level.  A thread-block cluster of CX x CY CTAs
+// (64x32 tile each, <= 16 CTAs, 1 per SM) holds an entire pyramid level on
+// chip and runs the whole _solve_level (optflow.py:147-214) in ONE launch:
+// bilinear upsample of the coarser flow (:244-249), then per warp the
+// linearisation (:158-176), all primal-dual iterations and the 3x3 median
+// (:210-211).  Tiles do not overlap: after every half step each CTA copies
+// its neighbours' edge rows/columns of the just-written field into its apron
+// through distributed shared memory (cluster.sync() + map_shared_rank), so
+// no halo is recomputed and no state leaves the chip until the level ends.
+// ------------------------------------------------------------------------
+struct LevelArgs {
+  const double *i0, *i1;  // x255 pyramid level of image 0; per-image stride ps
+  int64_t ps;
+  const double *ix, *iy;    // gradient of i1, [nb][cap]
+  const double *uc1, *uc2;  // coarser flow [nb][cap], null at the coarsest level
+  int wc, hc;
+  double rx, ry, sx, sy;  // wc/w, hc/h, w/wc, h/hc
+  double *uo1, *uo2;      // this level's flow out [nb][cap]
+  int w, h;
+  int64_t cap;
+  int warps, iters;
+  double tau, lam, sigma, shrink;
+};
+
+constexpr int kCTW = 64, kCBY = 16, kCPY = 2;  // 64 x 32 tile, 512 threads
+using CGeom = PDGeom<kCTW, kCBY, kCPY>;
+
+struct ClusterExchange {
+  double *sm;
+  int tid, bx, by, cx, cy;
+  // neighbour ranks (x fastest) or -1 outside the cluster
+  __device__ __forceinline__ int rank(int x, int y) const {
+    return (x < 0 || y < 0 || x >= cx || y >= cy) ? -1 : x + y * cx;
+  }
+  // copy `count` doubles at local offsets dst[k] <- neighbour's src[k]
+  __device__ __forceinline__ void pull(int nrank, int plane, int dst, int src, int dstride,
+                                       int sstride, int count, int t0) {
+    if (nrank < 0) return;
+    cg::cluster_group cl = cg::this_cluster();
+    double *mine = sm + plane * CGeom::PLANE;
+    const double *theirs = cl.map_shared_rank(mine, nrank);
+    for (int k = tid - t0; k >= 0 && k < count; k += 1 << 30) mine[dst + k * dstride] = theirs[src + k * sstride];
+  }
+  // p after the dual step: left apron column <- left neighbour's last column
+  // (p11, p21); top apron row <- upper neighbour's last row (p12, p22)
+  __device__ void after_dual() {
+    cg::this_cluster().sync();
+    constexpr int SP = CGeom::SP, TW = kCTW, TH = CGeom::TH;
+    const int l = rank(bx - 1, by), u = rank(bx, by - 1);
+    pull(l, 2, SP, SP + TW, SP, SP, TH, 0);               // p11 col
+    pull(l, 4, SP, SP + TW, SP, SP, TH, TH);              // p21 col
+    pull(u, 3, 1, TH * SP + 1, 1, 1, TW, 2 * TH);         // p12 row
+    pull(u, 5, 1, TH * SP + 1, 1, 1, TW, 2 * TH + TW);    // p22 row
+    __syncthreads();
+  }
+  // u-bar after the primal step: right apron column <- right neighbour's
+  // first column; bottom apron row <- lower neighbour's first row
+  __device__ void after_primal() {
+    cg::this_cluster().sync();
+    constexpr int SP = CGeom::SP, TW = kCTW, TH = CGeom::TH;
+    const int r = rank(bx + 1, by), d = rank(bx, by + 1);
+    pull(r, 0, SP + TW + 1, SP + 1, SP, SP, TH, 0);               // b1 col
+    pull(r, 1, SP + TW + 1, SP + 1, SP, SP, TH, TH);              // b2 col
+    pull(d, 0, (TH + 1) * SP + 1, SP + 1, 1, 1, TW, 2 * TH);      // b1 row
+    pull(d, 1, (TH + 1) * SP + 1, SP + 1, 1, 1, TW, 2 * TH + TW); // b2 row
+    __syncthreads();
+  }
+};
+
+__global__ void __launch_bounds__(32 * kCBY, 1) k_level_cluster(const LevelArgs a) {
+  constexpr int NX = CGeom::NX, TH = CGeom::TH, NP = CGeom::NP, SP = CGeom::SP;
+  constexpr int PL = CGeom::PLANE, TW = kCTW, BY = kCBY;
+  extern __shared__ __align__(16) double sm[];
+  const int W = a.w, H = a.h;
+  const int ox = blockIdx.x * TW, oy = blockIdx.y * TH;
+  const int64_t so = blockIdx.z * a.cap;
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
+  const int base = (ty + 1) * SP + tx + 1;
+  ClusterExchange xch{sm, tid, (int)blockIdx.x, (int)blockIdx.y, (int)gridDim.x, (int)gridDim.y};
+  double2 *const queue = reinterpret_cast<double2 *>(sm + 6 * PL) + ty * (2 * NP * 32);
+  const double *i0 = a.i0 + blockIdx.z * a.ps, *i1 = a.i1 + blockIdx.z * a.ps;
+
+  for (int k = tid; k < 6 * PL; k += 32 * BY) sm[k] = 0.0;  // aprons start finite
+  __syncthreads();
+
+  // ---- initial flow: zero at the coarsest level, else upsampled (:244-249)
+  double u1[NP], u2[NP];
+  unsigned fl[NP];
+#pragma unroll
+  for (int q = 0; q < NP; ++q) {
+    const int gc = ox + tx + 32 * (q % NX), gr = oy + ty + BY * (q / NX);
+    u1[q] = 0.0;
+    u2[q] = 0.0;
+    if (a.uc1 && gc < W && gr < H) {
+      const double x = ((double)gc + 0.5) * a.rx - 0.5;
+      const double y = ((double)gr + 0.5) * a.ry - 0.5;
+      u1[q] = bsample(a.uc1 + so, a.wc, a.hc, x, y) * a.sx;
+      u2[q] = bsample(a.uc2 + so, a.wc, a.hc, x, y) * a.sy;
+    }
+    fl[q] = (gc < W - 1 ? FL_R : 0u) | (gr < H - 1 ? FL_D : 0u) | (gc > 0 ? FL_L : 0u) |
+            (gc == W - 1 ? FL_LASTC : 0u) | (gr > 0 ? FL_U : 0u) | (gr == H - 1 ? FL_LASTR : 0u);
+  }
+
+  const double tl = a.tau * a.lam;
+  for (int wp = 0; wp < a.warps; ++wp) {
+    // ---- linearise at the current flow (:158-176); ub = u, p = 0
+    double gx[NP], gy[NP], r0[NP], thr[NP], ig2[NP];
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      const int gc = ox + tx + 32 * (q % NX), gr = oy + ty + BY * (q / NX);
+      double vgx = 0.0, vgy = 0.0, vr0 = 0.0;
+      if (gc < W && gr < H) {
+        const double mx = (double)gc + u1[q], my = (double)gr + u2[q];
+        const double v = bsample(i1, W, H, mx, my);
+        vgx = bsample(a.ix + so, W, H, mx, my);
+        vgy = bsample(a.iy + so, W, H, mx, my);
+        vr0 = v - i0[(int64_t)gr * W + gc] - vgx * u1[q] - vgy * u2[q];
+      }
+      gx[q] = vgx;
+      gy[q] = vgy;
+      r0[q] = vr0;
+      const double g2 = vgx * vgx + vgy * vgy;
+      const bool ok = g2 > 1e-12;
+      ig2[q] = ok ? 1.0 / (g2 > 1e-12 ? g2 : 1e-12) : 0.0;
+      thr[q] = tl * g2;
+      fl[q] = (fl[q] & ~(unsigned)FL_OK) | (ok ? FL_OK : 0u);
+      const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
+      sm[id] = u1[q];
+      sm[PL + id] = u2[q];
+#pragma unroll
+      for (int f = 2; f < 6; ++f) sm[f * PL + id] = 0.0;
+    }
+    xch.after_primal();  // publish u-bar edges before the first dual step
+
+    pd_iterate<kCTW, kCBY, kCPY>(a.iters, sm, base, tx, fl, u1, u2, gx, gy, r0, thr, ig2, a.tau,
+                                 tl, a.sigma, a.shrink, queue, xch);
+
+    // ---- 3x3 median of u1, u2 with replicated borders (:210-211).  The p
+    // planes are free now (no neighbour reads them after the last exchange).
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
+      sm[2 * PL + id] = u1[q];
+      sm[3 * PL + id] = u2[q];
+    }
+    cg::this_cluster().sync();
+    {  // apron ring incl. corners from the 8 neighbours
+      cg::cluster_group cl = cg::this_cluster();
+      for (int k = tid; k < 2 * (2 * TW + 2 * TH + 4); k += 32 * BY) {
+        const int plane = 2 + (k & 1);
+        const int e = k >> 1;
+        int lr, lc;  // apron cell in local coordinates (-1..TH, -1..TW)
+        if (e < TW) { lr = -1; lc = e; }
+        else if (e < 2 * TW) { lr = TH; lc = e - TW; }
+        else if (e < 2 * TW + TH) { lr = e - 2 * TW; lc = -1; }
+        else if (e < 2 * TW + 2 * TH) { lr = e - 2 * TW - TH; lc = TW; }
+        else { const int c = e - 2 * TW - 2 * TH; lr = (c & 2) ? TH : -1; lc = (c & 1) ? TW : -1; }
+        const int nx = lc < 0 ? -1 : (lc >= TW ? 1 : 0), ny = lr < 0 ? -1 : (lr >= TH ? 1 : 0);
+        const int nr = xch.rank(xch.bx + nx, xch.by + ny);
+        if (nr < 0) continue;
+        const int sr = lr - ny * TH, sc = lc - nx * TW;  // cell in the neighbour's frame
+        double *mine = sm + plane * PL;
+        mine[(lr + 1) * SP + lc + 1] = cl.map_shared_rank(mine, nr)[(sr + 1) * SP + sc + 1];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      const int gc = ox + tx + 32 * (q % NX), gr = oy + ty + BY * (q / NX);
+      if (gc >= W || gr >= H) continue;
+      double v1[9], v2[9];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const int rr = min(max(gr - 1 + i, 0), H - 1) - oy;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          const int cc = min(max(gc - 1 + j, 0), W - 1) - ox;
+          v1[i * 3 + j] = sm[2 * PL + (rr + 1) * SP + cc + 1];
+          v2[i * 3 + j] = sm[3 * PL + (rr + 1) * SP + cc + 1];
+        }
+      }
+      u1[q] = median9(v1);
+      u2[q] = median9(v2);
+    }
+    cg::this_cluster().sync();  // neighbours are done reading our u planes
+  }
+
+#pragma unroll
+  for (int q = 0; q < NP; ++q) {
+    const int gc = ox + tx + 32 * (q % NX), gr = oy + ty + BY * (q / NX);
+    if (gc >= W || gr >= H) continue;
+    a.uo1[so + (int64_t)gr * W + gc] = u1[q];
+    a.uo2[so + (int64_t)gr * W + gc] = u2[q];
+  }
+}
+
 // Launch configurations (tile width x height, threads, min CTAs/SM).
 struct PDConfig {
   int idx, tw, th, by;
@@ -666,6 +892,64 @@ PDPlan pd_plan(int w, int h) {
 }
 
 inline dim3 grid2d(int w, int h, int nb) { return dim3((w + 31) / 32, (h + 7) / 8, nb); }
+
+cudaLaunchConfig_t level_cluster_cfg(int w, int h, int nb, cudaStream_t s,
+                                     cudaLaunchAttribute *attr) {
+  const int cx = (w + kCTW - 1) / kCTW, cy = (h + CGeom::TH - 1) / CGeom::TH;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cx, cy, nb);
+  cfg.blockDim = dim3(32, kCBY, 1);
+  cfg.dynamicSmemBytes = CGeom::smem;
+  cfg.stream = s;
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cx;
+  attr[0].val.clusterDim.y = cy;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cfg;
+}
+
+int level_cluster_setup() {
+  static int done = 0;
+  if (done) return FT_OK;
+  FT_CUDA_TRY(cudaFuncSetAttribute(k_level_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed,
+                                   1));
+  FT_CUDA_TRY(cudaFuncSetAttribute(k_level_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)CGeom::smem));
+  done = 1;
+  return FT_OK;
+}
+
+// Can level w x h run as one cluster (<= 16 CTAs, schedulable)?  FT_CLUSTER=0
+// disables the path (tiled kernels for every level).
+bool cluster_level_ok(int w, int h) {
+  if (!env_int("FT_CLUSTER", 1)) return false;
+  const int cx = (w + kCTW - 1) / kCTW, cy = (h + CGeom::TH - 1) / CGeom::TH;
+  if (cx * cy > 16) return false;
+  static int cache[17][17];  // 0 unknown, 1 yes, 2 no
+  int &c = cache[cx][cy];
+  if (c == 0) {
+    c = 2;
+    if (level_cluster_setup() == FT_OK) {
+      cudaLaunchAttribute attr[1];
+      cudaLaunchConfig_t cfg = level_cluster_cfg(w, h, 1, nullptr, attr);
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, k_level_cluster, &cfg) == cudaSuccess && n > 0) c = 1;
+      cudaGetLastError();
+    }
+  }
+  return c == 1;
+}
+
+int launch_level_cluster(const LevelArgs &a, int nb, cudaStream_t s) {
+  FT_TRY(level_cluster_setup());
+  cudaLaunchAttribute attr[1];
+  cudaLaunchConfig_t cfg = level_cluster_cfg(a.w, a.h, nb, s, attr);
+  FT_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_level_cluster, a));
+  count_launch();
+  return FT_OK;
+}
 
 }  // namespace
 
@@ -754,6 +1038,42 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
   for (int lvl = scales - 1; lvl >= 0; --lvl) {
     const int w = lw[lvl], h = lh[lvl];
     StatePtrs st = state_ptrs(fw.st[cur], fw.nb, cap);
+    if (cluster_level_ok(w, h)) {  // whole level on chip, one launch
+      const double *i0 = pyr0 + loff[lvl];
+      const double *i1 = pyr1 + loff[lvl];
+      k_central_grad<<<grid2d(w, h, nb), blk, 0, s>>>(i1, w, h, pyr_stride, fw.ix, fw.iy, cap);
+      count_launch();
+      LevelArgs la;
+      la.i0 = i0;
+      la.i1 = i1;
+      la.ps = pyr_stride;
+      la.ix = fw.ix;
+      la.iy = fw.iy;
+      const bool coarsest = lvl == scales - 1;
+      la.uc1 = coarsest ? nullptr : st.p[U1];
+      la.uc2 = coarsest ? nullptr : st.p[U2];
+      la.wc = coarsest ? 0 : lw[lvl + 1];
+      la.hc = coarsest ? 0 : lh[lvl + 1];
+      la.rx = coarsest ? 0.0 : (double)la.wc / (double)w;
+      la.ry = coarsest ? 0.0 : (double)la.hc / (double)h;
+      la.sx = coarsest ? 0.0 : (double)w / (double)la.wc;
+      la.sy = coarsest ? 0.0 : (double)h / (double)la.hc;
+      cur = 1 - cur;
+      StatePtrs out = state_ptrs(fw.st[cur], fw.nb, cap);
+      la.uo1 = out.p[U1];
+      la.uo2 = out.p[U2];
+      la.w = w;
+      la.h = h;
+      la.cap = cap;
+      la.warps = p.warps;
+      la.iters = p.iters;
+      la.tau = p.tau;
+      la.lam = p.lam;
+      la.sigma = sigma;
+      la.shrink = shrink;
+      FT_TRY(launch_level_cluster(la, nb, s));
+      continue;
+    }
     if (lvl == scales - 1) {
       for (int b = 0; b < nb; ++b) {
         FT_CUDA_TRY(cudaMemsetAsync(st.p[U1] + b * cap, 0, (size_t)w * h * 8, s));

@@ -921,10 +921,12 @@ int level_cluster_setup() {
   return FT_OK;
 }
 
-// Can level w x h run as one cluster (<= 16 CTAs, schedulable)?  FT_CLUSTER=0
+// Can level w x h run as one cluster (<= 16 CTAs, schedulable)?  Opt-in with
+// FT_CLUSTER=1: on B200 the per-iteration latency of one 64x32 CTA makes it
+// slower than the tiled kernels (profiles/r01_launches_cluster.md); FT_CLUSTER=0
 // disables the path (tiled kernels for every level).
 bool cluster_level_ok(int w, int h) {
-  if (!env_int("FT_CLUSTER", 1)) return false;
+  if (!env_int("FT_CLUSTER", 0)) return false;
   const int cx = (w + kCTW - 1) / kCTW, cy = (h + CGeom::TH - 1) / CGeom::TH;
   if (cx * cy > 16) return false;
   static int cache[17][17];  // 0 unknown, 1 yes, 2 no

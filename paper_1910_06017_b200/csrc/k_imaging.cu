@@ -4,6 +4,9 @@
 // rof_denoise :109-125, structure_texture :128-144) and the grid stencils of
 // imageops.py (smooth_gaussian5 :12-23, decimate2 :26-29, forward_gradient
 // :32-38, divergence :41-50).  All batched: blockIdx.z selects the image.
+#include <algorithm>
+#include <cstdlib>
+
 #include "ft_internal.cuh"
 
 namespace ft {
@@ -149,6 +152,88 @@ __global__ void k_st_combine(const double *__restrict__ img, int w, int h, int64
   out[o] = m;
 }
 
+// ROF iterations, temporally blocked (same scheme as k_pd_tile): a 32x32
+// tile with `halo` overlap runs `iters` dual steps on chip; the two fields
+// read at a neighbour (p at x-1 / y-1 for the divergence, d at x+1 / y+1 for
+// the forward gradient) live in shared memory with a one-element apron,
+// img/weight and the own p in registers.  Exact inner region written back.
+constexpr int kRTW = 32, kRBY = 16, kRPY = 2, kRTH = kRBY * kRPY;
+constexpr int kRSP = kRTW + 2, kRPL = kRSP * (kRTH + 2);
+
+__global__ void __launch_bounds__(32 * kRBY, 2)
+    k_rof_tile(const double *__restrict__ img, int w, int h, int64_t is,
+               const double *__restrict__ px_in, const double *__restrict__ py_in,
+               double *__restrict__ px_out, double *__restrict__ py_out, int64_t ps,
+               double weight, double step, int halo, int iters, int first) {
+  __shared__ double s_px[kRPL], s_py[kRPL], s_d[kRPL];
+  const int step_x = kRTW - 2 * halo, step_y = kRTH - 2 * halo;
+  const int ox = blockIdx.x * step_x - halo, oy = blockIdx.y * step_y - halo;
+  img += blockIdx.z * is;
+  const int64_t po = blockIdx.z * ps;
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
+  for (int k = tid; k < kRPL; k += 32 * kRBY) {
+    s_px[k] = 0.0;
+    s_py[k] = 0.0;
+    s_d[k] = 0.0;
+  }
+  __syncthreads();
+  double iw[kRPY], px[kRPY], py[kRPY];
+  bool fR[kRPY], fD[kRPY], fL[kRPY], fLC[kRPY], fU[kRPY], fLR[kRPY];
+#pragma unroll
+  for (int k = 0; k < kRPY; ++k) {
+    const int gc = ox + tx, gr = oy + ty + kRBY * k;
+    const bool in = gc >= 0 && gc < w && gr >= 0 && gr < h;
+    const int64_t o = (int64_t)gr * w + gc;
+    iw[k] = in ? img[o] / weight : 0.0;  // img / weight (imaging.py:121)
+    px[k] = (in && !first) ? px_in[po + o] : 0.0;
+    py[k] = (in && !first) ? py_in[po + o] : 0.0;
+    fR[k] = gc < w - 1;
+    fD[k] = gr < h - 1;
+    fL[k] = gc > 0;
+    fLC[k] = gc == w - 1;
+    fU[k] = gr > 0;
+    fLR[k] = gr == h - 1;
+    const int id = (ty + kRBY * k + 1) * kRSP + tx + 1;
+    s_px[id] = px[k];
+    s_py[id] = py[k];
+  }
+  __syncthreads();
+  for (int it = 0; it < iters; ++it) {
+    double d[kRPY];
+#pragma unroll
+    for (int k = 0; k < kRPY; ++k) {  // d = divergence(p) - img/weight
+      const int id = (ty + kRBY * k + 1) * kRSP + tx + 1;
+      const double l = s_px[id - 1], u = s_py[id - kRSP];
+      const double dx = fL[k] ? (fLC[k] ? -l : px[k] - l) : px[k];
+      const double dy = fU[k] ? (fLR[k] ? -u : py[k] - u) : py[k];
+      d[k] = (dx + dy) - iw[k];
+      s_d[id] = d[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kRPY; ++k) {  // g = forward_gradient(d); p update
+      const int id = (ty + kRBY * k + 1) * kRSP + tx + 1;
+      const double gx = fR[k] ? s_d[id + 1] - d[k] : 0.0;
+      const double gy = fD[k] ? s_d[id + kRSP] - d[k] : 0.0;
+      const double norm = 1.0 + step * glibc_hypot(gx, gy);
+      px[k] = (px[k] + step * gx) / norm;
+      py[k] = (py[k] + step * gy) / norm;
+      s_px[id] = px[k];
+      s_py[id] = py[k];
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int k = 0; k < kRPY; ++k) {
+    const int lr = ty + kRBY * k, gc = ox + tx, gr = oy + lr;
+    if (gc < 0 || gc >= w || gr < 0 || gr >= h) continue;
+    if (tx < halo || tx >= kRTW - halo || lr < halo || lr >= kRTH - halo) continue;
+    const int64_t o = po + (int64_t)gr * w + gc;
+    px_out[o] = px[k];
+    py_out[o] = py[k];
+  }
+}
+
 int grid1d(int64_t n, int bs) {
   int64_t g = (n + bs - 1) / bs;
   if (g > 4 * kSMs * 8) g = 4 * kSMs * 8;
@@ -201,11 +286,31 @@ int launch_structure_texture(const double *img, int w, int h, int64_t is, double
   double *p[2][2] = {{ws, ws + n}, {ws + 2 * n, ws + 3 * n}};
   int cur = 0;
   dim3 blk(32, 8), grd((w + kRB - 1) / kRB, (h + kRB - 1) / kRB, nb);
-  for (int it = 0; it < iterations; ++it) {
-    k_rof_step<<<grd, blk, 0, s>>>(img, w, h, is, p[cur][0], p[cur][1], p[1 - cur][0],
-                                   p[1 - cur][1], wss, weight, step);
-    count_launch();
-    cur = 1 - cur;
+  const char *naive = getenv("FT_ROF_NAIVE");
+  if (naive && *naive == '1') {  // one launch per iteration (A/B reference)
+    for (int it = 0; it < iterations; ++it) {
+      k_rof_step<<<grd, blk, 0, s>>>(img, w, h, is, p[cur][0], p[cur][1], p[1 - cur][0],
+                                     p[1 - cur][1], wss, weight, step);
+      count_launch();
+      cur = 1 - cur;
+    }
+  } else {
+    const char *hv = getenv("FT_ROF_HALO");
+    const int halo_t = (hv && *hv) ? atoi(hv) : 4;
+    const bool resident = w <= kRTW && h <= kRTH;
+    const int halo = resident ? 0 : halo_t;
+    const int sx = kRTW - 2 * halo, sy = kRTH - 2 * halo;
+    const dim3 g(resident ? 1 : (w + sx - 1) / sx, resident ? 1 : (h + sy - 1) / sy, nb);
+    int done = 0;
+    while (done < iterations) {
+      const int k = resident ? iterations : std::min(halo, iterations - done);
+      k_rof_tile<<<g, dim3(32, kRBY), 0, s>>>(img, w, h, is, p[cur][0], p[cur][1], p[1 - cur][0],
+                                              p[1 - cur][1], wss, weight, step, halo, k,
+                                              done == 0);
+      count_launch();
+      cur = 1 - cur;
+      done += k;
+    }
   }
   dim3 g2((w + 31) / 32, (h + 7) / 8, nb);
   k_st_combine<<<g2, blk, 0, s>>>(img, w, h, is, p[cur][0], p[cur][1], wss, weight, blend, out,

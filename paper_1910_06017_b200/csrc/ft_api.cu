@@ -4,6 +4,7 @@
 // entry points run the per-frame step for many independent
 // streams in lockstep, captured once per variant into a CUDA graph.
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -18,6 +19,22 @@ namespace ft {
 
 thread_local std::string g_err;
 thread_local LaunchCounter *g_launch_counter = nullptr;
+PhaseTimer *g_phase = nullptr;
+
+void PhaseTimer::report() {
+  if (n < 2) return;
+  cudaEventSynchronize(ev[n - 1]);
+  float total = 0.f;
+  cudaEventElapsedTime(&total, ev[0], ev[n - 1]);
+  fprintf(stderr, "[ft phase timing] total %.3f ms\n", total);
+  for (int i = 1; i < n; ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+    fprintf(stderr, "  %-28s %9.3f ms  %5.1f%%\n", name[i], ms, 100.f * ms / total);
+  }
+  for (int i = 0; i < n; ++i) cudaEventDestroy(ev[i]);
+  n = 0;
+}
 
 void set_error(const std::string &msg) { g_err = msg; }
 int fail(int code, const std::string &msg) {
@@ -550,6 +567,7 @@ struct ft_tracker {
       dets = d_dets;
       in = d_in;
     }
+    phase_mark("start");
     // (1) preprocessing: ingest + pyramid to level L (imaging.py:75-95) + ST
     const double *img;
     if (L == 0) {
@@ -564,10 +582,13 @@ struct ft_tracker {
                                     (int64_t)lw[l] * lh[l], nullptr, 0, 1.0, S, s));
       img = d_chain[L];
     }
+    phase_mark("ingest+pyramid");
     FT_TRY(launch_structure_texture(img, PW, PH, P, cfg.rof_weight, cfg.rof_blend,
                                     cfg.rof_iterations, d_st, P, d_rofws, 4 * P, S, s, 0, 0.25));
+    phase_mark("structure_texture");
     // (2) flow pyramid of the current ST frame (x255, optflow.py:242-243)
     FT_TRY(build_flow_pyramid(d_st, P, geo, d_fchain, d_pyr_cur, geo.total, S, s));
+    phase_mark("flow pyramid");
     // (3) feature calculation: TV-L1 between previous and current frame
     if (has_prev) {
       FlowParamsD p{cfg.flow.data_weight, cfg.flow.time_step, cfg.flow.huber_epsilon,
@@ -578,6 +599,7 @@ struct ft_tracker {
     // (4) prediction, matching, update
     FT_TRY(launch_tracker_track(T, d_dx, d_dy, P, PW, PH, L, dets, in + 1, in, has_prev, d_out,
                                 d_nout, s));
+    phase_mark("predict+match+update");
     // the current pyramid becomes the previous one
     FT_CUDA_TRY(cudaMemcpyAsync(d_pyr_prev, d_pyr_cur, (size_t)S * geo.total * 8,
                                 cudaMemcpyDeviceToDevice, s));
@@ -592,6 +614,17 @@ struct ft_tracker {
   int run(bool has_prev, const uint8_t *luma, const ft_det *dets, const int32_t *in,
           bool host_io) {
     cudaStream_t s = stream;
+    const char *pt = getenv("FT_PHASE_TIMING");
+    if (pt && *pt == '1' && has_prev) {  // eager run with per-phase events
+      PhaseTimer timer;
+      timer.on = true;
+      timer.s = s;
+      g_phase = &timer;
+      const int rc = enqueue(s, has_prev, luma, dets, in, host_io);
+      g_phase = nullptr;
+      timer.report();
+      return rc;
+    }
     GraphKey key{has_prev ? 1 : 0, host_io ? nullptr : luma, host_io ? nullptr : dets,
                  host_io ? nullptr : in};
     auto it = graphs.find(key);

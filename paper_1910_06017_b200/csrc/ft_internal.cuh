@@ -83,6 +83,27 @@ inline void count_launch(int n = 1) {
   if (g_launch_counter) g_launch_counter->n += n;
 }
 
+// Optional phase timing (FT_PHASE_TIMING=1): the tracker runs eagerly and
+// records a CUDA event at every mark(); report() prints the gaps to stderr.
+struct PhaseTimer {
+  bool on = false;
+  cudaStream_t s = nullptr;
+  int n = 0;
+  cudaEvent_t ev[64];
+  const char *name[64];
+  void mark(const char *what) {
+    if (!on || n >= 64) return;
+    cudaEventCreate(&ev[n]);
+    cudaEventRecord(ev[n], s);
+    name[n++] = what;
+  }
+  void report();
+};
+extern PhaseTimer *g_phase;
+inline void phase_mark(const char *what) {
+  if (g_phase) g_phase->mark(what);
+}
+
 // ---------------------------------------------------------------- imaging
 // All batched launchers operate on `nb` independent images laid out with a
 // fixed element stride between consecutive images.

@@ -893,6 +893,10 @@ PDPlan pd_plan(int w, int h) {
 
 inline dim3 grid2d(int w, int h, int nb) { return dim3((w + 31) / 32, (h + 7) / 8, nb); }
 
+const char *const kLevelNames[8] = {"flow level 0", "flow level 1", "flow level 2",
+                                    "flow level 3", "flow level 4", "flow level 5",
+                                    "flow level 6", "flow level 7+"};
+
 cudaLaunchConfig_t level_cluster_cfg(int w, int h, int nb, cudaStream_t s,
                                      cudaLaunchAttribute *attr) {
   const int cx = (w + kCTW - 1) / kCTW, cy = (h + CGeom::TH - 1) / CGeom::TH;
@@ -1074,6 +1078,7 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
       la.sigma = sigma;
       la.shrink = shrink;
       FT_TRY(launch_level_cluster(la, nb, s));
+      phase_mark(kLevelNames[lvl < 8 ? lvl : 7]);
       continue;
     }
     if (lvl == scales - 1) {
@@ -1134,6 +1139,7 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
       count_launch();
       cur = 1 - cur;
     }
+    phase_mark(kLevelNames[lvl < 8 ? lvl : 7]);
   }
   StatePtrs st = state_ptrs(fw.st[cur], fw.nb, cap);
   const int64_t n0 = (int64_t)lw[0] * lh[0];

@@ -966,7 +966,9 @@ int profile_pd(FlowWork &fw, int w, int h, int nb, const FlowParamsD &p, int rep
                cudaStream_t s, double *ms_per_launch, int *iters_per_launch) {
   const PDPlan plan = pd_plan(w, h);
   const int halo = plan.halo;
-  const int iters = halo ? std::min(halo, p.iters) : p.iters;
+  // FT_PD_PROFILE_ITERS overrides the iterations per launch (cost model:
+  // load/store overhead vs per-iteration cost)
+  const int iters = env_int("FT_PD_PROFILE_ITERS", halo ? std::min(halo, p.iters) : p.iters);
   PDArgs a;
   a.gx = fw.gx;
   a.gy = fw.gy;

@@ -198,7 +198,7 @@ struct PDArgs {
   const double *gx, *gy, *r0;
   int w, h;
   int64_t cap;
-  int halo, iters, first;
+  int halo, iters, first, nb;
   double tau, lam, sigma, shrink;  // shrink = 1/(1+sigma*eps)
 };
 
@@ -817,12 +817,166 @@ __global__ void __launch_bounds__(32 * kCBY, 1) k_level_cluster(const LevelArgs 
   }
 }
 
+// ------------------------------------------------------------------------
+// Persistent, software-pipelined variant of k_pd_tile.  The launch cost of
+// the tiled kernel is (load+store, HBM-bound) + K x (iteration, issue-bound)
+// with almost no overlap between the two (tools/pd_cost_model.sh).  Here a
+// grid of one CTA per SM walks the tiles; while a CTA iterates on tile t its
+// threads' cp.async copies (LDGSTS, zero-fill outside the image) are already
+// streaming tile t+1 into a shared-memory staging buffer, and the interior of
+// tile t is written back with plain stores that drain during the next tile's
+// compute.  Every thread stages exactly the pixels it owns, so the hand-off
+// needs only its own cp.async.wait_group.
+// ------------------------------------------------------------------------
+constexpr int kNStage = 11;  // u1 u2 b1 b2 p11 p12 p21 p22 gx gy rho0
+
+template <int TW, int BY, int PY>
+struct PersistGeom {
+  using G = PDGeom<TW, BY, PY>;
+  static constexpr int TPX = TW * G::TH;  // pixels per tile
+  // exchange planes (no projection queue) + staging
+  static constexpr size_t smem = 6 * G::PLANE * sizeof(double) + kNStage * TPX * sizeof(double) +
+                                 BY * 2 * G::NP * 32 * 16;
+};
+
+__device__ __forceinline__ void cp_async8(double *dst, const double *src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const int n = valid ? 8 : 0;  // src-size 0: zero-fill the 8 bytes
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+template <int TW, int BY, int PY>
+__global__ void __launch_bounds__(32 * BY, 1) k_pd_persist(const PDArgs a) {
+  using G = PDGeom<TW, BY, PY>;
+  using PG = PersistGeom<TW, BY, PY>;
+  constexpr int NX = G::NX, TH = G::TH, NP = G::NP, SP = G::SP, PL = G::PLANE, TPX = PG::TPX;
+  extern __shared__ __align__(16) double sm[];
+  double *const stage = sm + 6 * PL;
+  double2 *const queue =
+      reinterpret_cast<double2 *>(stage + kNStage * TPX) + threadIdx.y * (2 * NP * 32);
+  const int W = a.w, H = a.h;
+  const int step_x = TW - 2 * a.halo, step_y = TH - 2 * a.halo;
+  const int ntx = a.halo ? (W + step_x - 1) / step_x : 1;
+  const int nty = a.halo ? (H + step_y - 1) / step_y : 1;
+  const int ntiles = ntx * nty * a.nb;
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
+  const int base = (ty + 1) * SP + tx + 1;
+  const int nload = a.first ? 5 : kNStage;  // first launch of a warp: u, gx, gy, rho0
+  const double tl = a.tau * a.lam;
+
+  for (int k = tid; k < 6 * PL; k += 32 * BY) sm[k] = 0.0;  // apron stays zero
+
+  auto tile_origin = [&](int t, int &ox, int &oy, int64_t &so) {
+    const int bz = t / (ntx * nty), r = t % (ntx * nty);
+    ox = (r % ntx) * step_x - a.halo;
+    oy = (r / ntx) * step_y - a.halo;
+    so = (int64_t)bz * a.cap;
+  };
+  // stage the pixels this thread owns; plane order: U1 U2 (B1 B2 P11..P22) gx gy r0
+  auto issue_loads = [&](int t) {
+    int ox, oy;
+    int64_t so;
+    tile_origin(t, ox, oy, so);
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      const int lc = tx + 32 * (q % NX), lr = ty + BY * (q / NX);
+      const int gc = ox + lc, gr = oy + lr;
+      const bool in = gc >= 0 && gc < W && gr >= 0 && gr < H;
+      const int64_t o = in ? so + (int64_t)gr * W + gc : 0;
+      const int li = lr * TW + lc;
+      cp_async8(stage + 0 * TPX + li, a.in.p[U1] + o, in);
+      cp_async8(stage + 1 * TPX + li, a.in.p[U2] + o, in);
+      if (!a.first) {
+#pragma unroll
+        for (int f = B1; f <= P22; ++f) cp_async8(stage + f * TPX + li, a.in.p[f] + o, in);
+      }
+      cp_async8(stage + 8 * TPX + li, a.gx + o, in);
+      cp_async8(stage + 9 * TPX + li, a.gy + o, in);
+      cp_async8(stage + 10 * TPX + li, a.r0 + o, in);
+    }
+    cp_async_commit();
+  };
+  (void)nload;
+
+  int t = blockIdx.x;
+  if (t < ntiles) issue_loads(t);
+  for (; t < ntiles; t += gridDim.x) {
+    int ox, oy;
+    int64_t so;
+    tile_origin(t, ox, oy, so);
+    cp_async_wait_all();  // this thread's staged pixels of tile t have landed
+    double u1[NP], u2[NP], gx[NP], gy[NP], r0[NP], thr[NP], ig2[NP];
+    unsigned fl[NP];
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      const int lc = tx + 32 * (q % NX), lr = ty + BY * (q / NX);
+      const int gc = ox + lc, gr = oy + lr;
+      const int li = lr * TW + lc;
+      u1[q] = stage[0 * TPX + li];
+      u2[q] = stage[1 * TPX + li];
+      gx[q] = stage[8 * TPX + li];
+      gy[q] = stage[9 * TPX + li];
+      r0[q] = stage[10 * TPX + li];
+      const double g2 = gx[q] * gx[q] + gy[q] * gy[q];  // optflow.py:163
+      const bool ok = g2 > 1e-12;
+      ig2[q] = ok ? 1.0 / (g2 > 1e-12 ? g2 : 1e-12) : 0.0;
+      thr[q] = tl * g2;
+      fl[q] = (gc < W - 1 ? FL_R : 0u) | (gr < H - 1 ? FL_D : 0u) | (gc > 0 ? FL_L : 0u) |
+              (gc == W - 1 ? FL_LASTC : 0u) | (gr > 0 ? FL_U : 0u) |
+              (gr == H - 1 ? FL_LASTR : 0u) | (ok ? FL_OK : 0u);
+      const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
+      if (a.first) {
+        sm[id] = u1[q];  // ub = u, p = 0 (optflow.py:169-174)
+        sm[PL + id] = u2[q];
+#pragma unroll
+        for (int f = 2; f < 6; ++f) sm[f * PL + id] = 0.0;
+      } else {
+#pragma unroll
+        for (int f = 0; f < 6; ++f) sm[f * PL + id] = stage[(2 + f) * TPX + li];
+      }
+    }
+    __syncthreads();  // exchange planes hold tile t (and tile t-1 is finished)
+    if (t + (int)gridDim.x < ntiles) issue_loads(t + gridDim.x);  // overlaps the compute
+
+    BlockBarrier bar;
+    pd_iterate<TW, BY, PY>(a.iters, sm, base, tx, fl, u1, u2, gx, gy, r0, thr, ig2, a.tau, tl,
+                           a.sigma, a.shrink, queue, bar);
+
+    // ---- write back the exact interior (drains during the next tile)
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      const int lc = tx + 32 * (q % NX), lr = ty + BY * (q / NX);
+      const int gc = ox + lc, gr = oy + lr;
+      if (gc < 0 || gc >= W || gr < 0 || gr >= H) continue;
+      if (lc < a.halo || lc >= TW - a.halo || lr < a.halo || lr >= TH - a.halo) continue;
+      const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
+      const int64_t o = so + (int64_t)gr * W + gc;
+      a.out.p[U1][o] = u1[q];
+      a.out.p[U2][o] = u2[q];
+#pragma unroll
+      for (int f = 0; f < 6; ++f) a.out.p[B1 + f][o] = sm[f * PL + id];
+    }
+  }
+}
+
 // Launch configurations (tile width x height, threads, min CTAs/SM).
 struct PDConfig {
   int idx, tw, th, by;
   void (*fn)(PDArgs);
   size_t smem;
+  bool persistent = false;
 };
+
+template <int TW, int BY, int PY>
+PDConfig make_persist_cfg(int idx) {
+  using G = PDGeom<TW, BY, PY>;
+  return PDConfig{idx, TW, G::TH, BY, &k_pd_persist<TW, BY, PY>, PersistGeom<TW, BY, PY>::smem,
+                  true};
+}
 
 template <int BY, int PY, int MINB>
 PDConfig make_strip_cfg(int idx) {
@@ -850,6 +1004,8 @@ inline PDConfig pd_config(int i) {
     case 9: return make_strip_cfg<16, 4, 1>(9);
     case 10: return make_cfg<32, 16, 2, 1>(10);
     case 11: return make_cfg<32, 32, 1, 1>(11);
+    case 12: return make_persist_cfg<32, 16, 2>(12);
+    case 13: return make_persist_cfg<32, 8, 4>(13);
     default: return make_cfg<32, 8, 4, 2>(0);
   }
 }
@@ -864,6 +1020,19 @@ int pd_launch(const PDConfig &c, const PDArgs &a, int nb, cudaStream_t s) {
   const int step_x = c.tw - 2 * a.halo, step_y = c.th - 2 * a.halo;
   const dim3 grid(a.halo ? (a.w + step_x - 1) / step_x : 1, a.halo ? (a.h + step_y - 1) / step_y : 1,
                   nb);
+  if (c.persistent) {  // one CTA per SM walking all tiles
+    static int sms = 0;
+    if (!sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if (sms <= 0) sms = kSMs;
+    }
+    const int ntiles = grid.x * grid.y * grid.z;
+    c.fn<<<ntiles < sms ? ntiles : sms, dim3(32, c.by), c.smem, s>>>(a);
+    count_launch();
+    return FT_OK;
+  }
   c.fn<<<grid, dim3(32, c.by), c.smem, s>>>(a);
   count_launch();
   return FT_OK;
@@ -979,6 +1148,7 @@ int profile_pd(FlowWork &fw, int w, int h, int nb, const FlowParamsD &p, int rep
   a.halo = halo;
   a.iters = iters;
   a.first = 0;
+  a.nb = nb;
   a.tau = p.tau;
   a.lam = p.lam;
   a.sigma = 1.0 / (8.0 * p.tau);
@@ -1126,6 +1296,7 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
         a.halo = halo;
         a.iters = n;
         a.first = done == 0;
+        a.nb = nb;
         a.tau = p.tau;
         a.lam = p.lam;
         a.sigma = sigma;

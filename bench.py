@@ -271,7 +271,11 @@ def run_ours(args, ws, rank, local):
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "pd_traffic.json")
     if os.path.exists(tfile):
-        traffic = json.load(open(tfile)).get("dram_bytes_per_launch")
+        tj = json.load(open(tfile))
+        # ncu capture of one finest-level launch, normalised per stream-pixel
+        # and rescaled to this run's streams (same kernel, same geometry)
+        if tj.get("bytes_per_stream_pixel"):
+            traffic = round(tj["bytes_per_stream_pixel"] * B * W_ * H_, 1)
     # step-level roofline: SURVEY 8(d) algorithmic bytes per SD frame (22.03 GB at C2)
     frame_bytes = 22.03e9
     step_frac = (value / ws) * frame_bytes / (hbm * 1e9)

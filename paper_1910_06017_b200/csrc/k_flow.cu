@@ -13,6 +13,7 @@
 //   state ping-pong st[2]           [8][nb][cap]  (u1 u2 b1 b2 p11 p12 p21 p22)
 // where b = "u bar" (optflow.py:173-174, :205-206).
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 
 #include <cooperative_groups.h>
@@ -199,6 +200,7 @@ struct PDArgs {
   int w, h;
   int64_t cap;
   int halo, iters, first, nb;
+  int pow2;  // sigma and tau are powers of two (exact fused multiply-adds)
   double tau, lam, sigma, shrink;  // shrink = 1/(1+sigma*eps)
 };
 
@@ -217,7 +219,16 @@ struct PDGeom {
 // exchange planes with apron) and registers (pointwise fields); `xch` runs
 // after each half step's shared-memory writes (a block barrier in the tiled
 // kernel, the DSMEM edge exchange in the cluster kernel).
-template <int TW, int BY, int PY, typename X>
+// a*b + c.  With P2 the product is exact (b or a is a power of two: sigma
+// and tau for the default time_step 0.25, the literal 2.0), so one fused
+// multiply-add rounds exactly like the reference's separate multiply and
+// add; otherwise the two IEEE operations are kept (-fmad=false).
+template <bool P2>
+__device__ __forceinline__ double madx(double a, double b, double c) {
+  return P2 ? fma(a, b, c) : a * b + c;
+}
+
+template <int TW, int BY, int PY, bool P2, typename X>
 __device__ __forceinline__ void pd_iterate(int iters, double *sm, int base, int tx,
                                            const unsigned *fl, double *u1, double *u2,
                                            const double *gx, const double *gy, const double *r0,
@@ -243,10 +254,10 @@ __device__ __forceinline__ void pd_iterate(int iters, double *sm, int base, int 
       const double a1y = D ? d1 - c1 : 0.0;
       const double a2x = R ? r2 - c2 : 0.0;
       const double a2y = D ? d2 - c2 : 0.0;
-      p11[q] = (sp11[id] + sigma * a1x) * shrink;
-      p12[q] = (sp12[id] + sigma * a1y) * shrink;
-      p21[q] = (sp21[id] + sigma * a2x) * shrink;
-      p22[q] = (sp22[id] + sigma * a2y) * shrink;
+      p11[q] = madx<P2>(sigma, a1x, sp11[id]) * shrink;
+      p12[q] = madx<P2>(sigma, a1y, sp12[id]) * shrink;
+      p21[q] = madx<P2>(sigma, a2x, sp21[id]) * shrink;
+      p22[q] = madx<P2>(sigma, a2y, sp22[id]) * shrink;
     }
     // ---- unit-ball projection n = max(1, hypot(.)); p /= n (:186-191).
     // When |q|^2 is clearly below 1 the norm is exactly 1 and p/1 == p, so
@@ -257,8 +268,9 @@ __device__ __forceinline__ void pd_iterate(int iters, double *sm, int base, int 
       unsigned need = 0;
 #pragma unroll
       for (int q = 0; q < NP; ++q) {
-        if (p11[q] * p11[q] + p12[q] * p12[q] > 0.999999) need |= 1u << (2 * q);
-        if (p21[q] * p21[q] + p22[q] * p22[q] > 0.999999) need |= 1u << (2 * q + 1);
+        // screening test only (not reference arithmetic): fused is fine
+        if (fma(p11[q], p11[q], p12[q] * p12[q]) > 0.999999) need |= 1u << (2 * q);
+        if (fma(p21[q], p21[q], p22[q] * p22[q]) > 0.999999) need |= 1u << (2 * q + 1);
       }
       int off[2 * NP];
       int total = 0;
@@ -318,8 +330,8 @@ __device__ __forceinline__ void pd_iterate(int iters, double *sm, int base, int 
       const double dx2 = L ? (LC ? -l21 : p21[q] - l21) : p21[q];
       const double dy1 = U ? (LR ? -u12 : p12[q] - u12) : p12[q];
       const double dy2 = U ? (LR ? -u22 : p22[q] - u22) : p22[q];
-      const double v1 = u1[q] + tau * (dx1 + dy1);
-      const double v2 = u2[q] + tau * (dx2 + dy2);
+      const double v1 = madx<P2>(tau, dx1 + dy1, u1[q]);
+      const double v2 = madx<P2>(tau, dx2 + dy2, u2[q]);
       const double rho = r0[q] + gx[q] * v1 + gy[q] * v2;
       const bool lo = rho < -thr[q];
       const bool hi = rho > thr[q];
@@ -327,8 +339,8 @@ __device__ __forceinline__ void pd_iterate(int iters, double *sm, int base, int 
       d = ((f & FL_OK) || lo || hi) ? d : 0.0;
       const double n1 = v1 + d * gx[q];
       const double n2 = v2 + d * gy[q];
-      sb1[id] = 2.0 * n1 - u1[q];  // in place: no other thread reads u-bar here
-      sb2[id] = 2.0 * n2 - u2[q];
+      sb1[id] = madx<true>(2.0, n1, -u1[q]);  // in place: no other thread reads u-bar here
+      sb2[id] = madx<true>(2.0, n2, -u2[q]);
       u1[q] = n1;
       u2[q] = n2;
     }
@@ -427,8 +439,12 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const PDArgs a) {
 
   double2 *const queue = reinterpret_cast<double2 *>(sm + 6 * PL) + ty * (2 * NP * 32);
   BlockBarrier bar;
-  pd_iterate<TW, BY, PY>(a.iters, sm, base, tx, fl, u1, u2, gx, gy, r0, thr, ig2, a.tau, tl,
-                         a.sigma, a.shrink, queue, bar);
+  if (a.pow2)
+    pd_iterate<TW, BY, PY, true>(a.iters, sm, base, tx, fl, u1, u2, gx, gy, r0, thr, ig2, a.tau,
+                                 tl, a.sigma, a.shrink, queue, bar);
+  else
+    pd_iterate<TW, BY, PY, false>(a.iters, sm, base, tx, fl, u1, u2, gx, gy, r0, thr, ig2, a.tau,
+                                  tl, a.sigma, a.shrink, queue, bar);
 
   // ---- write back the exact interior
   const int lo_x = a.halo, hi_x = TW - a.halo;
@@ -755,7 +771,7 @@ __global__ void __launch_bounds__(32 * kCBY, 1) k_level_cluster(const LevelArgs 
     }
     xch.after_primal();  // publish u-bar edges before the first dual step
 
-    pd_iterate<kCTW, kCBY, kCPY>(a.iters, sm, base, tx, fl, u1, u2, gx, gy, r0, thr, ig2, a.tau,
+    pd_iterate<kCTW, kCBY, kCPY, false>(a.iters, sm, base, tx, fl, u1, u2, gx, gy, r0, thr, ig2, a.tau,
                                  tl, a.sigma, a.shrink, queue, xch);
 
     // ---- 3x3 median of u1, u2 with replicated borders (:210-211).  The p
@@ -943,8 +959,12 @@ __global__ void __launch_bounds__(32 * BY, 1) k_pd_persist(const PDArgs a) {
     if (t + (int)gridDim.x < ntiles) issue_loads(t + gridDim.x);  // overlaps the compute
 
     BlockBarrier bar;
-    pd_iterate<TW, BY, PY>(a.iters, sm, base, tx, fl, u1, u2, gx, gy, r0, thr, ig2, a.tau, tl,
-                           a.sigma, a.shrink, queue, bar);
+    if (a.pow2)
+      pd_iterate<TW, BY, PY, true>(a.iters, sm, base, tx, fl, u1, u2, gx, gy, r0, thr, ig2,
+                                   a.tau, tl, a.sigma, a.shrink, queue, bar);
+    else
+      pd_iterate<TW, BY, PY, false>(a.iters, sm, base, tx, fl, u1, u2, gx, gy, r0, thr, ig2,
+                                    a.tau, tl, a.sigma, a.shrink, queue, bar);
 
     // ---- write back the exact interior (drains during the next tile)
 #pragma unroll
@@ -1060,6 +1080,12 @@ PDPlan pd_plan(int w, int h) {
   return PDPlan{pd_config(env_int("FT_PD_CFG", 1)), env_int("FT_PD_HALO", 3)};
 }
 
+// tau = 2^k (then sigma = 1/(8 tau) = 2^(-k-3) too): products by them are exact
+inline int pow2_params(double tau) {
+  int e = 0;
+  return tau > 0.0 && std::frexp(tau, &e) == 0.5 ? 1 : 0;
+}
+
 inline dim3 grid2d(int w, int h, int nb) { return dim3((w + 31) / 32, (h + 7) / 8, nb); }
 
 const char *const kLevelNames[8] = {"flow level 0", "flow level 1", "flow level 2",
@@ -1149,6 +1175,7 @@ int profile_pd(FlowWork &fw, int w, int h, int nb, const FlowParamsD &p, int rep
   a.iters = iters;
   a.first = 0;
   a.nb = nb;
+  a.pow2 = pow2_params(p.tau);
   a.tau = p.tau;
   a.lam = p.lam;
   a.sigma = 1.0 / (8.0 * p.tau);
@@ -1297,6 +1324,7 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
         a.iters = n;
         a.first = done == 0;
         a.nb = nb;
+        a.pow2 = pow2_params(p.tau);
         a.tau = p.tau;
         a.lam = p.lam;
         a.sigma = sigma;

@@ -5,6 +5,7 @@
 // imageops.py (smooth_gaussian5 :12-23, decimate2 :26-29, forward_gradient
 // :32-38, divergence :41-50).  All batched: blockIdx.z selects the image.
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 
 #include "ft_internal.cuh"
@@ -160,6 +161,7 @@ __global__ void k_st_combine(const double *__restrict__ img, int w, int h, int64
 constexpr int kRTW = 32, kRBY = 16, kRPY = 2, kRTH = kRBY * kRPY;
 constexpr int kRSP = kRTW + 2, kRPL = kRSP * (kRTH + 2);
 
+template <bool P2>
 __global__ void __launch_bounds__(32 * kRBY, 2)
     k_rof_tile(const double *__restrict__ img, int w, int h, int64_t is,
                const double *__restrict__ px_in, const double *__restrict__ py_in,
@@ -215,9 +217,12 @@ __global__ void __launch_bounds__(32 * kRBY, 2)
       const int id = (ty + kRBY * k + 1) * kRSP + tx + 1;
       const double gx = fR[k] ? s_d[id + 1] - d[k] : 0.0;
       const double gy = fD[k] ? s_d[id + kRSP] - d[k] : 0.0;
-      const double norm = 1.0 + step * glibc_hypot(gx, gy);
-      px[k] = (px[k] + step * gx) / norm;
-      py[k] = (py[k] + step * gy) / norm;
+      // step = 2^k (default 0.25): step*x is exact, so the fused forms round
+      // exactly like the reference's separate multiply and add
+      const double hy = glibc_hypot(gx, gy);
+      const double norm = P2 ? fma(step, hy, 1.0) : 1.0 + step * hy;
+      px[k] = (P2 ? fma(step, gx, px[k]) : px[k] + step * gx) / norm;
+      py[k] = (P2 ? fma(step, gy, py[k]) : py[k] + step * gy) / norm;
       s_px[id] = px[k];
       s_py[id] = py[k];
     }
@@ -304,9 +309,11 @@ int launch_structure_texture(const double *img, int w, int h, int64_t is, double
     int done = 0;
     while (done < iterations) {
       const int k = resident ? iterations : std::min(halo, iterations - done);
-      k_rof_tile<<<g, dim3(32, kRBY), 0, s>>>(img, w, h, is, p[cur][0], p[cur][1], p[1 - cur][0],
-                                              p[1 - cur][1], wss, weight, step, halo, k,
-                                              done == 0);
+      int e2 = 0;
+      const bool p2 = step > 0.0 && std::frexp(step, &e2) == 0.5;
+      auto kern = p2 ? k_rof_tile<true> : k_rof_tile<false>;
+      kern<<<g, dim3(32, kRBY), 0, s>>>(img, w, h, is, p[cur][0], p[cur][1], p[1 - cur][0],
+                                        p[1 - cur][1], wss, weight, step, halo, k, done == 0);
       count_launch();
       cur = 1 - cur;
       done += k;

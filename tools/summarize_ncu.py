@@ -106,6 +106,8 @@ def main():
     ap.add_argument("--report")
     ap.add_argument("--tag", default="r01")
     ap.add_argument("--note", default="")
+    ap.add_argument("--stream-pixels", type=float, default=0.0,
+                    help="streams x pixels of the captured launch (normalises traffic)")
     a = ap.parse_args()
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     if a.launches:
@@ -117,9 +119,11 @@ def main():
         open(os.path.join(ROOT, "profiles", f"{a.tag}_pd_full.md"), "w").write(
             f"# {a.tag}: ncu --set full of the dominant kernel\n\n{a.note}\n\n{md}\n")
         if traffic is not None:
-            json.dump({"dram_bytes_per_launch": traffic, "grid": grid, "source": a.report,
-                       "tag": a.tag}, open(os.path.join(ROOT, "profiles", "pd_traffic.json"), "w"),
-                      indent=1)
+            rec = {"dram_bytes_per_launch": traffic, "grid": grid, "source": a.report,
+                   "tag": a.tag, "note": a.note}
+            if a.stream_pixels:
+                rec["bytes_per_stream_pixel"] = traffic / a.stream_pixels
+            json.dump(rec, open(os.path.join(ROOT, "profiles", "pd_traffic.json"), "w"), indent=1)
     print("ok")
 
 

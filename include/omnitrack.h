@@ -89,6 +89,13 @@ int ft_rof_denoise(ft_ctx *ctx, const double *d_in, int w, int h, double weight,
 int ft_compute_flow(ft_ctx *ctx, const double *d_prev, const double *d_curr, int w, int h,
                     const ft_flow_params *params, double *d_dx, double *d_dy);
 
+/* per-pixel terms of flow_energy (optflow.py:121-144): data = |I1(x+u)-I0|
+ * on x255 intensities, s1/s2 = huber(|forward_gradient(u_k)|); the
+ * reference's scalar is lambda*sum(data) + sum(s1) + sum(s2) in numpy order */
+int ft_flow_energy_terms(ft_ctx *ctx, const double *d_prev, const double *d_curr,
+                         const double *d_dx, const double *d_dy, int w, int h,
+                         double huber_epsilon, double *d_data, double *d_s1, double *d_s2);
+
 /* ---- tracking (track.py / assoc.py) ------------------------------------- */
 /* predict (track.py:56-87).  h_boxes: n x (x,y,w,h); field (d_dx,d_dy) is
  * field_w x field_h at pyramid `level`; h_out n x 4, h_valid[i]=0 for None */

@@ -322,6 +322,22 @@ int ft_compute_flow(ft_ctx *ctx, const double *prev, const double *curr, int w, 
                   dy, 0, 1, ctx->stream);
 }
 
+int ft_flow_energy_terms(ft_ctx *ctx, const double *prev, const double *curr, const double *dx,
+                         const double *dy, int w, int h, double huber_epsilon, double *data,
+                         double *s1, double *s2) {
+  if (!ctx || !prev || !curr || !dx || !dy || !data || !s1 || !s2)
+    return fail(FT_EINVAL, "NULL argument");
+  if (w < 1 || h < 1) return fail(FT_EINVAL, "empty field");
+  DeviceGuard g(ctx->device);
+  const int64_t n = (int64_t)w * h;
+  FT_TRY(ctx->ensure_scratch((size_t)2 * n * 8));
+  double *i0 = (double *)ctx->scratch, *i1 = i0 + n;
+  // flow_energy scales the frames by INTENSITY_SCALE first (optflow.py:143)
+  FT_TRY(launch_scale_copy(prev, n, 0, i0, 0, 255.0, 1, ctx->stream));
+  FT_TRY(launch_scale_copy(curr, n, 0, i1, 0, 255.0, 1, ctx->stream));
+  return launch_energy_terms(i0, i1, dx, dy, w, h, huber_epsilon, data, s1, s2, ctx->stream);
+}
+
 int ft_predict(ft_ctx *ctx, const double *h_boxes, int n, const double *dx, const double *dy,
                int fw_l, int fh_l, int level, int frame_w, int frame_h, double *h_out,
                uint8_t *h_valid) {

@@ -160,6 +160,9 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
              const int *lh, const int64_t *loff, int scales, const FlowParamsD &p, FlowWork &fw,
              double *dx, double *dy, int64_t out_stride, int nb, cudaStream_t s);
 
+int launch_energy_terms(const double *i0, const double *i1, const double *u1, const double *u2,
+                        int w, int h, double eps, double *data, double *s1, double *s2,
+                        cudaStream_t s);
 int profile_pd(FlowWork &fw, int w, int h, int nb, const FlowParamsD &p, int reps,
                cudaStream_t s, double *ms_per_launch, int *iters_per_launch);
 

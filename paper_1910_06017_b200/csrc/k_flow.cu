@@ -168,6 +168,33 @@ __global__ void k_median(const double *__restrict__ a1, const double *__restrict
   o2[so + (int64_t)r * w + c] = median9(v);
 }
 
+// Per-pixel terms of the TV-L1 objective (optflow.py:121-137): data term
+// |I1(x+u) - I0| and, per component, huber(hypot(forward_gradient(u))).
+// The reference sums these arrays with numpy; the caller does exactly that
+// on the host copies, so the scalar is bit-identical too.
+__global__ void k_energy_terms(const double *__restrict__ i0, const double *__restrict__ i1,
+                               const double *__restrict__ u1, const double *__restrict__ u2,
+                               int w, int h, double eps, double *__restrict__ data,
+                               double *__restrict__ s1, double *__restrict__ s2) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = blockIdx.y * blockDim.y + threadIdx.y;
+  if (r >= h || c >= w) return;
+  const int64_t o = (int64_t)r * w + c;
+  const double v = bsample(i1, w, h, (double)c + u1[o], (double)r + u2[o]);
+  data[o] = fabs(v - i0[o]);
+  const double *comp[2] = {u1, u2};
+  double *dst[2] = {s1, s2};
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const double *u = comp[k];
+    const double gx = c < w - 1 ? u[o + 1] - u[o] : 0.0;
+    const double gy = r < h - 1 ? u[o + w] - u[o] : 0.0;
+    const double m = glibc_hypot(gx, gy);
+    // _huber (optflow.py:121-124)
+    dst[k][o] = eps <= 0.0 ? m : (m <= eps ? m * m / (2.0 * eps) : m - eps / 2.0);
+  }
+}
+
 StatePtrs state_ptrs(double *base, int nb, int64_t cap) {
   StatePtrs s;
   for (int k = 0; k < NST; ++k) s.p[k] = base + (int64_t)k * nb * cap;
@@ -1354,4 +1381,16 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
   return FT_OK;
 }
 
+}  // namespace ft
+
+namespace ft {
+int launch_energy_terms(const double *i0, const double *i1, const double *u1, const double *u2,
+                        int w, int h, double eps, double *data, double *s1, double *s2,
+                        cudaStream_t s) {
+  k_energy_terms<<<dim3((w + 31) / 32, (h + 7) / 8), dim3(32, 8), 0, s>>>(i0, i1, u1, u2, w, h, eps,
+                                                                       data, s1, s2);
+  count_launch();
+  FT_CUDA_TRY(cudaGetLastError());
+  return FT_OK;
+}
 }  // namespace ft

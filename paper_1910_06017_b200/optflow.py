@@ -123,6 +123,56 @@ def auto_scales(width: int, height: int) -> int:
     return out.value
 
 
+FLO_MAGIC = 202021.25  # Middlebury .flo tag ("PIEH" as little-endian float)
+
+
+def flow_energy(prev: Frame, curr: Frame, field: MotionField,
+                params: FlowParams = FlowParams()) -> float:
+    """TV-L1 objective of `field` for a frame pair (optflow.py:140-144): the
+    per-pixel terms come from the device (ft_flow_energy_terms, bit-exact);
+    they are summed with numpy exactly as the reference sums its arrays."""
+    import torch
+
+    a, b = prev.device(), curr.device()
+    fdx, fdy = field.device()
+    data = torch.empty_like(a)
+    s1 = torch.empty_like(a)
+    s2 = torch.empty_like(a)
+    _lib.check(_lib.load().ft_flow_energy_terms(
+        _lib.ctx(), _lib.ptr(a), _lib.ptr(b), _lib.ptr(fdx), _lib.ptr(fdy), prev.width,
+        prev.height, float(params.huber_epsilon), _lib.ptr(data), _lib.ptr(s1), _lib.ptr(s2)))
+    total = params.data_weight * float(data.cpu().numpy().sum())
+    for term in (s1, s2):
+        total += float(term.cpu().numpy().sum())
+    return total
+
+
+def write_flo(field: MotionField, path) -> None:
+    """Middlebury .flo: tag, width, height, then float32 (dx, dy) pairs."""
+    inter = np.stack([field.dx, field.dy], axis=-1).astype(np.float32)
+    with open(path, "wb") as fh:
+        fh.write(np.array([FLO_MAGIC], "<f4").tobytes())
+        fh.write(np.array([field.width, field.height], "<i4").tobytes())
+        fh.write(inter.tobytes())
+
+
+def read_flo(path) -> MotionField:
+    with open(path, "rb") as fh:
+        head = fh.read(12)
+        if len(head) != 12:
+            raise ValueError(f"{path}: truncated .flo header")
+        magic = float(np.frombuffer(head[:4], "<f4")[0])
+        width, height = (int(v) for v in np.frombuffer(head[4:], "<i4"))
+        if abs(magic - FLO_MAGIC) > 1e-3:
+            raise ValueError(f"{path}: bad .flo magic {magic}")
+        body = fh.read(width * height * 8)
+        if len(body) != width * height * 8:
+            raise ValueError(f"{path}: truncated .flo data")
+    pairs = np.frombuffer(body, "<f4").reshape(height, width, 2)
+    return MotionField(width, height, pairs[..., 0].astype(np.float64),
+                       pairs[..., 1].astype(np.float64))
+
+
 def compute_flow(prev: Frame, curr: Frame, params: FlowParams = FlowParams(),
                  energy_trace: list | None = None) -> MotionField:
     """Coarse-to-fine TV-L1 from prev to curr (optflow.py:217-253).

@@ -189,3 +189,60 @@ class Tracker:
         _lib.check(self._lib.ft_tracker_launches(self._h, C.byref(c)))
         return c.value
 
+
+
+# ---------------------------------------------------------------------------
+# Outputs
+# ---------------------------------------------------------------------------
+def track_records(scene, frame_index: int) -> list:
+    """TrackRecord rows for one frame: every Active object plus the objects
+    that turned Lost on this frame."""
+    rows = []
+    for o in scene:
+        if o.state == ACTIVE or o.lost_at == frame_index:
+            x, y, w, h = o.box
+            rows.append({"frame": frame_index, "id": o.id, "class_id": o.class_id,
+                         "label": o.label, "x": x, "y": y, "w": w, "h": h, "score": o.score,
+                         "state": o.state})
+    return rows
+
+
+def write_jsonl(rows, fh) -> None:
+    import json
+    for r in rows:
+        fh.write(json.dumps(r) + "\n")
+
+
+def write_mot(rows, fh) -> None:
+    """MOTChallenge CSV: frame+1, id+1, x, y, w, h, score, -1, -1, -1."""
+    for r in rows:
+        fh.write(f"{r['frame'] + 1},{r['id'] + 1},{r['x']!r},{r['y']!r},{r['w']!r},{r['h']!r},"
+                 f"{r['score']!r},-1,-1,-1\n")
+
+
+def read_mot(fh) -> list:
+    """Inverse of write_mot (labels/state are not part of the format)."""
+    rows = []
+    for line in fh:
+        if not line.strip():
+            continue
+        f, i, x, y, w, h, s = line.split(",")[:7]
+        rows.append({"frame": int(f) - 1, "id": int(i) - 1, "x": float(x), "y": float(y),
+                     "w": float(w), "h": float(h), "score": float(s)})
+    return rows
+
+
+def run(frames, source, width: int, height: int, detect_every: int = 1, **tracker_kw):
+    """Drive a single-stream Tracker over an iterable of u8 luma frames with
+    a DetectionSource.  Frames whose index is not a
+    multiple of `detect_every` have no detector result (coast).  Yields
+    (frame_index, scene) per frame."""
+    trk = Tracker(width, height, n_streams=1, **tracker_kw)
+    try:
+        for t, luma in enumerate(frames):
+            if hasattr(luma, "data") and not isinstance(luma, np.ndarray):
+                luma = np.rint(np.asarray(luma.data) * 255.0).astype(np.uint8)
+            dets = source.lookup(t) if t % detect_every == 0 else None
+            yield t, trk.step(luma, t, [dets])[0]
+    finally:
+        trk.close()

@@ -1,8 +1,19 @@
-"""Scene-object lifecycle on the B200 (drop-in for reference track.py:
-SceneObject, active_set, predict, update).
+"""Track records and their per-frame lifecycle, executed on the B200.
 
-predict() runs the segmented box-mean kernel on the device field; update()
-runs the lifecycle kernel (ft_update).  Objects stay immutable host records.
+Drop-in for the reference's track module (track.py): the record type
+`SceneObject`, `active_set`, `predict` and `update` keep their names,
+arguments, defaults and exceptions.  The arithmetic runs in libomnitrack:
+
+* predict -> ft_predict: per box a warp evaluates the rounded, clamped pixel
+  support and the exact numpy-order mean of the flow inside it
+  (track.py:56-87);
+* update  -> ft_update: the match-driven transition kernel
+  (track.py:90-139) -- matched boxes take the detection (or a blend),
+  unmatched Active records turn Lost, unmatched detections spawn records
+  with fresh ids above every id ever issued.
+
+Records are immutable host values; only their numeric fields cross the
+C ABI (labels stay on the host).
 """
 from __future__ import annotations
 
@@ -18,14 +29,26 @@ ACTIVE = "active"
 LOST = "lost"
 
 
+def _validated_box(state, born_at, last_seen, box):
+    # same checks and messages as the reference record (track.py:35-44)
+    if state not in (ACTIVE, LOST):
+        raise ValueError(f"unknown state {state!r}")
+    if last_seen < born_at:
+        raise ValueError("last_seen cannot precede born_at")
+    bx, by, bw, bh = (float(v) for v in box)
+    if bw <= 0 or bh <= 0:
+        raise ValueError(f"box must have positive size, got {box[2]}x{box[3]}")
+    return bx, by, bw, bh
+
+
 @dataclass(frozen=True)
 class SceneObject:
-    """A persistent tracked entity in original-frame coordinates (track.py:21-44)."""
+    """One tracked entity, box in original-frame pixels (x, y, w, h)."""
 
     id: int
     class_id: int
     label: str
-    box: tuple  # x, y, w, h
+    box: tuple
     state: str = ACTIVE
     born_at: int = 0
     last_seen: int = 0
@@ -33,96 +56,96 @@ class SceneObject:
     lost_at: int | None = None
 
     def __post_init__(self):
-        if self.state not in (ACTIVE, LOST):
-            raise ValueError(f"unknown state {self.state!r}")
-        if self.last_seen < self.born_at:
-            raise ValueError("last_seen cannot precede born_at")
-        x, y, w, h = self.box
-        if w <= 0 or h <= 0:
-            raise ValueError(f"box must have positive size, got {w}x{h}")
-        object.__setattr__(self, "box", (float(x), float(y), float(w), float(h)))
+        object.__setattr__(self, "box",
+                           _validated_box(self.state, self.born_at, self.last_seen, self.box))
 
 
 def active_set(objects) -> list:
-    """Objects still eligible for prediction and matching, order kept."""
-    return [o for o in objects if o.state == ACTIVE]
+    """The records that still take part in prediction and matching."""
+    return [rec for rec in objects if rec.state == ACTIVE]
+
+
+def _box_array(records) -> np.ndarray:
+    arr = np.array([r.box for r in records], dtype=np.float64).reshape(-1, 4)
+    return np.ascontiguousarray(arr)
 
 
 def predict(objects, field: MotionField, level: int, frame_size) -> list:
-    """Shift each box by the mean flow over its rounded support (track.py:56-87).
+    """Move every box by the mean motion over its support at pyramid `level`.
 
-    One entry per object: the shifted (x, y, w, h), or None when the box has
-    no pixel support left.
+    Returns, per record, the new (x, y, w, h) -- size unchanged, position
+    clamped into the frame -- or None when the rounded support is empty.
+    Lost records are rejected with ValueError, as in the reference.
     """
-    objects = list(objects)
-    for o in objects:
-        if o.state != ACTIVE:
-            raise ValueError(f"cannot predict lost object {o.id}")
-    n = len(objects)
-    if n == 0:
+    records = list(objects)
+    lost = next((r for r in records if r.state != ACTIVE), None)
+    if lost is not None:
+        raise ValueError(f"cannot predict lost object {lost.id}")
+    if not records:
         return []
-    fw, fh = frame_size
-    boxes = np.ascontiguousarray(np.array([o.box for o in objects], dtype=np.float64))
-    out = np.empty((n, 4), dtype=np.float64)
-    valid = np.empty(n, dtype=np.uint8)
-    ddx, ddy = field.device()
-    _lib.check(_lib.load().ft_predict(_lib.ctx(), _lib.ptr(boxes), n, _lib.ptr(ddx),
-                                      _lib.ptr(ddy), field.width, field.height, int(level),
-                                      int(fw), int(fh), _lib.ptr(out), _lib.ptr(valid)))
-    return [tuple(float(v) for v in out[i]) if valid[i] else None for i in range(n)]
+    width, height = frame_size
+    src = _box_array(records)
+    dst = np.empty_like(src)
+    ok = np.empty(len(records), dtype=np.uint8)
+    fdx, fdy = field.device()
+    _lib.check(_lib.load().ft_predict(
+        _lib.ctx(), _lib.ptr(src), len(records), _lib.ptr(fdx), _lib.ptr(fdy), field.width,
+        field.height, int(level), int(width), int(height), _lib.ptr(dst), _lib.ptr(ok)))
+    return [tuple(map(float, dst[k])) if ok[k] else None for k in range(len(records))]
+
+
+# flags returned per existing record by ft_update
+_KEEP, _MATCHED, _TURNED_LOST = 0, 1, 2
 
 
 def update(objects, assignment, detections, frame_index: int,
            detection_blend: float = 1.0) -> list:
-    """Apply one frame's match results (track.py:90-139): matched objects take
-    the detection's box (or a blend) and score, unmatched Active objects turn
-    Lost, every unmatched detection spawns a new object with a fresh id."""
-    objects = list(objects)
-    detections = list(detections)
-    n, nd = len(objects), len(detections)
-    pairs = []
-    for i, j, _ in assignment.pairs:
-        if not 0 <= i < n:
+    """One frame of the lifecycle (see module docstring); returns a new list:
+    the existing records in order, then one spawned record per unmatched
+    detection in detection order."""
+    records = list(objects)
+    dets = list(detections)
+    n_rec, n_det = len(records), len(dets)
+    pairs = np.array([(i, j) for i, j, _ in assignment.pairs], dtype=np.int32).reshape(-1, 2)
+    for i, j in pairs:  # index errors first, like the reference's first loop
+        if not 0 <= i < n_rec:
             raise IndexError(f"scene index {i} out of range")
-        if not 0 <= j < nd:
+        if not 0 <= j < n_det:
             raise IndexError(f"detection index {j} out of range")
-        pairs.append((i, j))
-    matched = {i for i, _ in pairs}
-    for i in sorted(matched):
-        if objects[i].state != ACTIVE:
-            raise ValueError(f"lost object {objects[i].id} appeared in the assignment")
-    ids = np.array([o.id for o in objects], dtype=np.int64)
-    state = np.array([1 if o.state == ACTIVE else 0 for o in objects], dtype=np.int32)
-    boxes = np.array([o.box for o in objects], dtype=np.float64).reshape(-1, 4)
-    dboxes = np.array([d.box for d in detections], dtype=np.float64).reshape(-1, 4)
-    pr = np.array(pairs, dtype=np.int32).reshape(-1, 2)
-    out_src = np.empty(n + nd, dtype=np.int32)    # >=0 object index, <0: -(det+1) spawn
-    out_box = np.empty((n + nd, 4), dtype=np.float64)
-    out_flag = np.empty(n + nd, dtype=np.int32)   # 0 keep, 1 matched, 2 -> lost
-    out_id = np.empty(n + nd, dtype=np.int64)
-    cnt = C.c_int()
+    matched_to = {int(i): int(j) for i, j in pairs}
+    for i in sorted(matched_to):
+        if records[i].state != ACTIVE:
+            raise ValueError(f"lost object {records[i].id} appeared in the assignment")
+
+    ids = np.array([r.id for r in records], dtype=np.int64)
+    active = np.array([r.state == ACTIVE for r in records], dtype=np.int32)
+    rows = n_rec + n_det
+    src = np.empty(rows, dtype=np.int32)
+    boxes = np.empty((rows, 4), dtype=np.float64)
+    flags = np.empty(rows, dtype=np.int32)
+    new_ids = np.empty(rows, dtype=np.int64)
+    count = C.c_int()
     _lib.check(_lib.load().ft_update(
-        _lib.ctx(), _lib.ptr(ids), _lib.ptr(state), _lib.ptr(np.ascontiguousarray(boxes)), n,
-        _lib.ptr(pr), len(pr), _lib.ptr(np.ascontiguousarray(dboxes)), nd,
-        float(detection_blend), _lib.ptr(out_src), _lib.ptr(out_box), _lib.ptr(out_flag),
-        _lib.ptr(out_id), C.byref(cnt)))
-    result = []
-    for k in range(cnt.value):
-        src = int(out_src[k])
-        if src >= 0:
-            o = objects[src]
-            flag = int(out_flag[k])
-            if flag == 1:
-                j = dict(pairs)[src]
-                result.append(replace(o, box=tuple(float(v) for v in out_box[k]),
-                                      score=detections[j].score, last_seen=frame_index))
-            elif flag == 2:
-                result.append(replace(o, state=LOST, lost_at=frame_index))
-            else:
-                result.append(o)
+        _lib.ctx(), _lib.ptr(ids), _lib.ptr(active), _lib.ptr(_box_array(records)), n_rec,
+        _lib.ptr(pairs), len(pairs), _lib.ptr(_box_array(dets)), n_det, float(detection_blend),
+        _lib.ptr(src), _lib.ptr(boxes), _lib.ptr(flags), _lib.ptr(new_ids), C.byref(count)))
+
+    out = []
+    for row in range(count.value):
+        k = int(src[row])
+        if k < 0:  # spawn from detection -k-1
+            det = dets[-k - 1]
+            out.append(SceneObject(id=int(new_ids[row]), class_id=det.class_id, label=det.label,
+                                   box=det.box, state=ACTIVE, born_at=frame_index,
+                                   last_seen=frame_index, score=det.score))
+            continue
+        rec = records[k]
+        flag = int(flags[row])
+        if flag == _MATCHED:
+            out.append(replace(rec, box=tuple(map(float, boxes[row])),
+                               score=dets[matched_to[k]].score, last_seen=frame_index))
+        elif flag == _TURNED_LOST:
+            out.append(replace(rec, state=LOST, lost_at=frame_index))
         else:
-            d = detections[-src - 1]
-            result.append(SceneObject(id=int(out_id[k]), class_id=d.class_id, label=d.label,
-                                      box=d.box, state=ACTIVE, born_at=frame_index,
-                                      last_seen=frame_index, score=d.score))
-    return result
+            out.append(rec)
+    return out

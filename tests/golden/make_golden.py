@@ -260,8 +260,44 @@ def gen_step():
         save(f"step_{name}.npz", **out)
 
 
+def gen_io():
+    """video_io parsing (PGM with comments, PPM -> luma, Y4M 420) and optflow
+    diagnostics (flow_energy, .flo bytes) from the reference."""
+    import tempfile
+
+    from flowtrack import video_io
+    rng = np.random.default_rng(51)
+    out = {}
+    g = rng.integers(0, 256, (7, 9), dtype=np.uint8)
+    pgm = b"P5\n# made by make_golden\n9 7\n# max\n255\n" + g.tobytes()
+    rgb = rng.integers(0, 256, (5, 6, 3), dtype=np.uint8)
+    ppm = b"P6 6 5 255\n" + rgb.tobytes()
+    ys = [rng.integers(0, 256, (6, 10), dtype=np.uint8) for _ in range(3)]
+    y4m = b"YUV4MPEG2 W10 H6 F25:1 Ip A1:1 C420jpeg\n"
+    for y in ys:
+        y4m += b"FRAME\n" + y.tobytes() + bytes(2 * 5 * 3)
+    with tempfile.TemporaryDirectory() as d:
+        for name, blob in (("a.pgm", pgm), ("b.ppm", ppm), ("c.y4m", y4m)):
+            open(os.path.join(d, name), "wb").write(blob)
+        out["pgm_bytes"] = np.frombuffer(pgm, np.uint8)
+        out["pgm_want"] = video_io.read_pgm(os.path.join(d, "a.pgm"))
+        out["ppm_bytes"] = np.frombuffer(ppm, np.uint8)
+        out["ppm_want"] = video_io.read_pgm(os.path.join(d, "b.ppm"))
+        out["y4m_bytes"] = np.frombuffer(y4m, np.uint8)
+        out["y4m_want"] = np.stack([f.data for f in video_io.iter_y4m(os.path.join(d, "c.y4m"))])
+        z = np.load(os.path.join(HERE, "flow.npz"))
+        pa = imaging.Frame.from_array(z["f0_sta"])
+        pb = imaging.Frame.from_array(z["f0_stb"], 1)
+        fld = optflow.MotionField(width=pa.width, height=pa.height, dx=z["f0_dx"], dy=z["f0_dy"])
+        out["energy"] = np.array([optflow.flow_energy(pa, pb, fld),
+                                  optflow.flow_energy(pa, pb, fld, optflow.FlowParams(huber_epsilon=0.0))])
+        optflow.write_flo(fld, os.path.join(d, "f.flo"))
+        out["flo_bytes"] = np.frombuffer(open(os.path.join(d, "f.flo"), "rb").read(), np.uint8)
+    save("io.npz", **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["imaging", "flow", "predict", "assoc", "step"]
+    which = sys.argv[1:] or ["imaging", "flow", "predict", "assoc", "step", "io"]
     for w in which:
         globals()[f"gen_{w}"]()
         print("wrote", w)

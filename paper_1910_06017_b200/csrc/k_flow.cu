@@ -234,6 +234,17 @@ struct PDArgs {
 // per-pixel border flags (global position, fixed for the launch)
 enum : unsigned { FL_R = 1, FL_D = 2, FL_L = 4, FL_LASTC = 8, FL_U = 16, FL_LASTR = 32, FL_OK = 64 };
 
+// Exchange planes hold the fields read at a neighbour as three interleaved
+// double2 planes -- (b1,b2), (p11,p21), (p12,p22) -- the pairs that are always
+// read together, so each neighbour access is one 128-bit shared load.  sxi()
+// maps field f (0..5 = b1 b2 p11 p12 p21 p22) of element id to its double
+// index.
+__device__ __forceinline__ int sxi(int f, int id, int PL) {
+  const int pair = f == 0 || f == 1 ? 0 : (f == 2 || f == 4 ? 1 : 2);
+  const int comp = f == 1 || f == 4 || f == 5 ? 1 : 0;
+  return 2 * (pair * PL + id) + comp;
+}
+
 template <int TW, int BY, int PY>
 struct PDGeom {
   static constexpr int NX = TW / 32, TH = BY * PY, NP = NX * PY;
@@ -264,8 +275,7 @@ __device__ __forceinline__ void pd_iterate(int iters, double *sm, int base, int 
                                            X &xch) {
   using G = PDGeom<TW, BY, PY>;
   constexpr int NX = G::NX, NP = G::NP, SP = G::SP, PL = G::PLANE;
-  double *const sb1 = sm, *const sb2 = sm + PL, *const sp11 = sm + 2 * PL;
-  double *const sp12 = sm + 3 * PL, *const sp21 = sm + 4 * PL, *const sp22 = sm + 5 * PL;
+  double2 *const sB = reinterpret_cast<double2 *>(sm), *const sPX = sB + PL, *const sPY = sPX + PL;
   const unsigned lt_mask = (1u << tx) - 1u;
   for (int it = 0; it < iters; ++it) {
     double p11[NP], p12[NP], p21[NP], p22[NP];
@@ -274,17 +284,18 @@ __device__ __forceinline__ void pd_iterate(int iters, double *sm, int base, int 
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
       const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
-      const double c1 = sb1[id], c2 = sb2[id];
-      const double r1 = sb1[id + 1], r2 = sb2[id + 1], d1 = sb1[id + SP], d2 = sb2[id + SP];
+      const double2 cb = sB[id], rb = sB[id + 1], db = sB[id + SP];
+      const double2 opx = sPX[id], opy = sPY[id];
+      const double c1 = cb.x, c2 = cb.y, r1 = rb.x, r2 = rb.y, d1 = db.x, d2 = db.y;
       const bool R = fl[q] & FL_R, D = fl[q] & FL_D;
       const double a1x = R ? r1 - c1 : 0.0;
       const double a1y = D ? d1 - c1 : 0.0;
       const double a2x = R ? r2 - c2 : 0.0;
       const double a2y = D ? d2 - c2 : 0.0;
-      p11[q] = madx<P2>(sigma, a1x, sp11[id]) * shrink;
-      p12[q] = madx<P2>(sigma, a1y, sp12[id]) * shrink;
-      p21[q] = madx<P2>(sigma, a2x, sp21[id]) * shrink;
-      p22[q] = madx<P2>(sigma, a2y, sp22[id]) * shrink;
+      p11[q] = madx<P2>(sigma, a1x, opx.x) * shrink;
+      p12[q] = madx<P2>(sigma, a1y, opy.x) * shrink;
+      p21[q] = madx<P2>(sigma, a2x, opx.y) * shrink;
+      p22[q] = madx<P2>(sigma, a2y, opy.y) * shrink;
     }
     // ---- unit-ball projection n = max(1, hypot(.)); p /= n (:186-191).
     // When |q|^2 is clearly below 1 the norm is exactly 1 and p/1 == p, so
@@ -338,10 +349,8 @@ __device__ __forceinline__ void pd_iterate(int iters, double *sm, int base, int 
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
       const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
-      sp11[id] = p11[q];  // in place: no other thread reads p in this phase
-      sp12[id] = p12[q];
-      sp21[id] = p21[q];
-      sp22[id] = p22[q];
+      sPX[id] = make_double2(p11[q], p21[q]);  // in place: only the owner reads p here
+      sPY[id] = make_double2(p12[q], p22[q]);
     }
     xch.after_dual();
     // ---- primal descent + TV-L1 shrinkage (:194-208)
@@ -350,8 +359,8 @@ __device__ __forceinline__ void pd_iterate(int iters, double *sm, int base, int 
       const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
       const unsigned f = fl[q];
       // divergence (imageops.py:41-50): dx + dy with border rules
-      const double l11 = sp11[id - 1], l21 = sp21[id - 1];
-      const double u12 = sp12[id - SP], u22 = sp22[id - SP];
+      const double2 lp = sPX[id - 1], up = sPY[id - SP];
+      const double l11 = lp.x, l21 = lp.y, u12 = up.x, u22 = up.y;
       const bool L = f & FL_L, LC = f & FL_LASTC, U = f & FL_U, LR = f & FL_LASTR;
       const double dx1 = L ? (LC ? -l11 : p11[q] - l11) : p11[q];
       const double dx2 = L ? (LC ? -l21 : p21[q] - l21) : p21[q];
@@ -366,8 +375,8 @@ __device__ __forceinline__ void pd_iterate(int iters, double *sm, int base, int 
       d = ((f & FL_OK) || lo || hi) ? d : 0.0;
       const double n1 = v1 + d * gx[q];
       const double n2 = v2 + d * gy[q];
-      sb1[id] = madx<true>(2.0, n1, -u1[q]);  // in place: no other thread reads u-bar here
-      sb2[id] = madx<true>(2.0, n2, -u2[q]);
+      // in place: no other thread reads u-bar in this phase
+      sB[id] = make_double2(madx<true>(2.0, n1, -u1[q]), madx<true>(2.0, n2, -u2[q]));
       u1[q] = n1;
       u2[q] = n2;
     }
@@ -386,8 +395,6 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const PDArgs a) {
   using G = PDGeom<TW, BY, PY>;
   constexpr int NX = G::NX, TH = G::TH, NP = G::NP, SP = G::SP, PL = G::PLANE;
   extern __shared__ __align__(16) double sm[];
-  double *const sb1 = sm, *const sb2 = sm + PL, *const sp11 = sm + 2 * PL;
-  double *const sp12 = sm + 3 * PL, *const sp21 = sm + 4 * PL, *const sp22 = sm + 5 * PL;
 
   const int W = a.w, H = a.h;
   const int step_x = TW - 2 * a.halo, step_y = TH - 2 * a.halo;
@@ -406,7 +413,7 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const PDArgs a) {
     else if (k < 2 * SP + TH) idx = (k - 2 * SP + 1) * SP;
     else idx = (k - 2 * SP - TH + 1) * SP + SP - 1;
 #pragma unroll
-    for (int f = 0; f < 6; ++f) sm[f * PL + idx] = 0.0;
+    for (int f = 0; f < 6; ++f) sm[sxi(f, idx, PL)] = 0.0;
   }
 
   const double tl = a.tau * a.lam;
@@ -454,12 +461,12 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const PDArgs a) {
               (gc == W - 1 ? FL_LASTC : 0u) | (gr > 0 ? FL_U : 0u) | (gr == H - 1 ? FL_LASTR : 0u) |
               (ok ? FL_OK : 0u);
       const int id = base + k * BY * SP + 32 * cx;
-      sb1[id] = vb1;
-      sb2[id] = vb2;
-      sp11[id] = q11;
-      sp12[id] = q12;
-      sp21[id] = q21;
-      sp22[id] = q22;
+      sm[sxi(0, id, PL)] = vb1;
+      sm[sxi(1, id, PL)] = vb2;
+      sm[sxi(2, id, PL)] = q11;
+      sm[sxi(3, id, PL)] = q12;
+      sm[sxi(4, id, PL)] = q21;
+      sm[sxi(5, id, PL)] = q22;
     }
   }
   __syncthreads();
@@ -487,12 +494,8 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const PDArgs a) {
     const int64_t o = so + (int64_t)gr * W + gc;
     a.out.p[U1][o] = u1[q];
     a.out.p[U2][o] = u2[q];
-    a.out.p[B1][o] = sb1[id];
-    a.out.p[B2][o] = sb2[id];
-    a.out.p[P11][o] = sp11[id];
-    a.out.p[P12][o] = sp12[id];
-    a.out.p[P21][o] = sp21[id];
-    a.out.p[P22][o] = sp22[id];
+#pragma unroll
+    for (int f = 0; f < 6; ++f) a.out.p[B1 + f][o] = sm[sxi(f, id, PL)];
   }
 }
 
@@ -703,9 +706,11 @@ struct ClusterExchange {
                                        int sstride, int count, int t0) {
     if (nrank < 0) return;
     cg::cluster_group cl = cg::this_cluster();
-    double *mine = sm + plane * CGeom::PLANE;
-    const double *theirs = cl.map_shared_rank(mine, nrank);
-    for (int k = tid - t0; k >= 0 && k < count; k += 1 << 30) mine[dst + k * dstride] = theirs[src + k * sstride];
+    const double *theirs = cl.map_shared_rank(sm, nrank);
+    const int k = tid - t0;  // field `plane` = b1 b2 p11 p12 p21 p22 index
+    if (k >= 0 && k < count)
+      sm[sxi(plane, dst + k * dstride, CGeom::PLANE)] =
+          theirs[sxi(plane, src + k * sstride, CGeom::PLANE)];
   }
   // p after the dual step: left apron column <- left neighbour's last column
   // (p11, p21); top apron row <- upper neighbour's last row (p12, p22)
@@ -746,7 +751,7 @@ __global__ void __launch_bounds__(32 * kCBY, 1) k_level_cluster(const LevelArgs 
   double2 *const queue = reinterpret_cast<double2 *>(sm + 6 * PL) + ty * (2 * NP * 32);
   const double *i0 = a.i0 + blockIdx.z * a.ps, *i1 = a.i1 + blockIdx.z * a.ps;
 
-  for (int k = tid; k < 6 * PL; k += 32 * BY) sm[k] = 0.0;  // aprons start finite
+  for (int k = tid; k < 6 * PL; k += 32 * BY) sm[k] = 0.0;  // aprons start finite (all planes)
   __syncthreads();
 
   // ---- initial flow: zero at the coarsest level, else upsampled (:244-249)
@@ -791,10 +796,10 @@ __global__ void __launch_bounds__(32 * kCBY, 1) k_level_cluster(const LevelArgs 
       thr[q] = tl * g2;
       fl[q] = (fl[q] & ~(unsigned)FL_OK) | (ok ? FL_OK : 0u);
       const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
-      sm[id] = u1[q];
-      sm[PL + id] = u2[q];
+      sm[sxi(0, id, PL)] = u1[q];
+      sm[sxi(1, id, PL)] = u2[q];
 #pragma unroll
-      for (int f = 2; f < 6; ++f) sm[f * PL + id] = 0.0;
+      for (int f = 2; f < 6; ++f) sm[sxi(f, id, PL)] = 0.0;
     }
     xch.after_primal();  // publish u-bar edges before the first dual step
 
@@ -806,8 +811,8 @@ __global__ void __launch_bounds__(32 * kCBY, 1) k_level_cluster(const LevelArgs 
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
       const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
-      sm[2 * PL + id] = u1[q];
-      sm[3 * PL + id] = u2[q];
+      sm[sxi(2, id, PL)] = u1[q];
+      sm[sxi(3, id, PL)] = u2[q];
     }
     cg::this_cluster().sync();
     {  // apron ring incl. corners from the 8 neighbours
@@ -825,8 +830,8 @@ __global__ void __launch_bounds__(32 * kCBY, 1) k_level_cluster(const LevelArgs 
         const int nr = xch.rank(xch.bx + nx, xch.by + ny);
         if (nr < 0) continue;
         const int sr = lr - ny * TH, sc = lc - nx * TW;  // cell in the neighbour's frame
-        double *mine = sm + plane * PL;
-        mine[(lr + 1) * SP + lc + 1] = cl.map_shared_rank(mine, nr)[(sr + 1) * SP + sc + 1];
+        sm[sxi(plane, (lr + 1) * SP + lc + 1, PL)] =
+            cl.map_shared_rank(sm, nr)[sxi(plane, (sr + 1) * SP + sc + 1, PL)];
       }
     }
     __syncthreads();
@@ -841,8 +846,8 @@ __global__ void __launch_bounds__(32 * kCBY, 1) k_level_cluster(const LevelArgs 
 #pragma unroll
         for (int j = 0; j < 3; ++j) {
           const int cc = min(max(gc - 1 + j, 0), W - 1) - ox;
-          v1[i * 3 + j] = sm[2 * PL + (rr + 1) * SP + cc + 1];
-          v2[i * 3 + j] = sm[3 * PL + (rr + 1) * SP + cc + 1];
+          v1[i * 3 + j] = sm[sxi(2, (rr + 1) * SP + cc + 1, PL)];
+          v2[i * 3 + j] = sm[sxi(3, (rr + 1) * SP + cc + 1, PL)];
         }
       }
       u1[q] = median9(v1);
@@ -973,13 +978,13 @@ __global__ void __launch_bounds__(32 * BY, 1) k_pd_persist(const PDArgs a) {
               (gr == H - 1 ? FL_LASTR : 0u) | (ok ? FL_OK : 0u);
       const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
       if (a.first) {
-        sm[id] = u1[q];  // ub = u, p = 0 (optflow.py:169-174)
-        sm[PL + id] = u2[q];
+        sm[sxi(0, id, PL)] = u1[q];  // ub = u, p = 0 (optflow.py:169-174)
+        sm[sxi(1, id, PL)] = u2[q];
 #pragma unroll
-        for (int f = 2; f < 6; ++f) sm[f * PL + id] = 0.0;
+        for (int f = 2; f < 6; ++f) sm[sxi(f, id, PL)] = 0.0;
       } else {
 #pragma unroll
-        for (int f = 0; f < 6; ++f) sm[f * PL + id] = stage[(2 + f) * TPX + li];
+        for (int f = 0; f < 6; ++f) sm[sxi(f, id, PL)] = stage[(2 + f) * TPX + li];
       }
     }
     __syncthreads();  // exchange planes hold tile t (and tile t-1 is finished)
@@ -1005,7 +1010,7 @@ __global__ void __launch_bounds__(32 * BY, 1) k_pd_persist(const PDArgs a) {
       a.out.p[U1][o] = u1[q];
       a.out.p[U2][o] = u2[q];
 #pragma unroll
-      for (int f = 0; f < 6; ++f) a.out.p[B1 + f][o] = sm[f * PL + id];
+      for (int f = 0; f < 6; ++f) a.out.p[B1 + f][o] = sm[sxi(f, id, PL)];
     }
   }
 }

@@ -125,9 +125,10 @@ def update(objects, assignment, detections, frame_index: int,
     flags = np.empty(rows, dtype=np.int32)
     new_ids = np.empty(rows, dtype=np.int64)
     count = C.c_int()
+    rec_boxes, det_boxes = _box_array(records), _box_array(dets)  # alive across the call
     _lib.check(_lib.load().ft_update(
-        _lib.ctx(), _lib.ptr(ids), _lib.ptr(active), _lib.ptr(_box_array(records)), n_rec,
-        _lib.ptr(pairs), len(pairs), _lib.ptr(_box_array(dets)), n_det, float(detection_blend),
+        _lib.ctx(), _lib.ptr(ids), _lib.ptr(active), _lib.ptr(rec_boxes), n_rec,
+        _lib.ptr(pairs), len(pairs), _lib.ptr(det_boxes), n_det, float(detection_blend),
         _lib.ptr(src), _lib.ptr(boxes), _lib.ptr(flags), _lib.ptr(new_ids), C.byref(count)))
 
     out = []

@@ -266,7 +266,10 @@ __device__ __forceinline__ double madx(double a, double b, double c) {
   return P2 ? fma(a, b, c) : a * b + c;
 }
 
-template <int TW, int BY, int PY, bool P2, typename X>
+// IN: the tile holds no image-border pixel (all border rules are "interior":
+// the reference's zero gradients / one-sided divergences never apply), so the
+// per-pixel flag selects fold away.
+template <int TW, int BY, int PY, bool P2, bool IN, typename X>
 __device__ __forceinline__ void pd_iterate(int iters, double *sm, int base, int tx,
                                            const unsigned *fl, double *u1, double *u2,
                                            const double *gx, const double *gy, const double *r0,
@@ -287,7 +290,7 @@ __device__ __forceinline__ void pd_iterate(int iters, double *sm, int base, int 
       const double2 cb = sB[id], rb = sB[id + 1], db = sB[id + SP];
       const double2 opx = sPX[id], opy = sPY[id];
       const double c1 = cb.x, c2 = cb.y, r1 = rb.x, r2 = rb.y, d1 = db.x, d2 = db.y;
-      const bool R = fl[q] & FL_R, D = fl[q] & FL_D;
+      const bool R = IN || (fl[q] & FL_R), D = IN || (fl[q] & FL_D);
       const double a1x = R ? r1 - c1 : 0.0;
       const double a1y = D ? d1 - c1 : 0.0;
       const double a2x = R ? r2 - c2 : 0.0;
@@ -312,11 +315,13 @@ __device__ __forceinline__ void pd_iterate(int iters, double *sm, int base, int 
       }
       int off[2 * NP];
       int total = 0;
+      if (__any_sync(0xffffffffu, need != 0u)) {  // most warps skip the queue
 #pragma unroll
-      for (int j = 0; j < 2 * NP; ++j) {
-        const unsigned m = __ballot_sync(0xffffffffu, (need >> j) & 1u);
-        off[j] = total + __popc(m & lt_mask);
-        total += __popc(m);
+        for (int j = 0; j < 2 * NP; ++j) {
+          const unsigned m = __ballot_sync(0xffffffffu, (need >> j) & 1u);
+          off[j] = total + __popc(m & lt_mask);
+          total += __popc(m);
+        }
       }
       if (total) {  // warp-uniform
 #pragma unroll
@@ -361,7 +366,8 @@ __device__ __forceinline__ void pd_iterate(int iters, double *sm, int base, int 
       // divergence (imageops.py:41-50): dx + dy with border rules
       const double2 lp = sPX[id - 1], up = sPY[id - SP];
       const double l11 = lp.x, l21 = lp.y, u12 = up.x, u22 = up.y;
-      const bool L = f & FL_L, LC = f & FL_LASTC, U = f & FL_U, LR = f & FL_LASTR;
+      const bool L = IN || (f & FL_L), LC = !IN && (f & FL_LASTC);
+      const bool U = IN || (f & FL_U), LR = !IN && (f & FL_LASTR);
       const double dx1 = L ? (LC ? -l11 : p11[q] - l11) : p11[q];
       const double dx2 = L ? (LC ? -l21 : p21[q] - l21) : p21[q];
       const double dy1 = U ? (LR ? -u12 : p12[q] - u12) : p12[q];
@@ -372,7 +378,7 @@ __device__ __forceinline__ void pd_iterate(int iters, double *sm, int base, int 
       const bool lo = rho < -thr[q];
       const bool hi = rho > thr[q];
       double d = lo ? tl : (hi ? -tl : -rho * ig2[q]);
-      d = ((f & FL_OK) || lo || hi) ? d : 0.0;
+      d = (ig2[q] != 0.0 || lo || hi) ? d : 0.0;  // ig2 != 0 <=> |grad|^2 > 1e-12
       const double n1 = v1 + d * gx[q];
       const double n2 = v2 + d * gy[q];
       // in place: no other thread reads u-bar in this phase
@@ -473,12 +479,17 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const PDArgs a) {
 
   double2 *const queue = reinterpret_cast<double2 *>(sm + 6 * PL) + ty * (2 * NP * 32);
   BlockBarrier bar;
-  if (a.pow2)
-    pd_iterate<TW, BY, PY, true>(a.iters, sm, base, tx, fl, u1, u2, gx, gy, r0, thr, ig2, a.tau,
-                                 tl, a.sigma, a.shrink, queue, bar);
-  else
-    pd_iterate<TW, BY, PY, false>(a.iters, sm, base, tx, fl, u1, u2, gx, gy, r0, thr, ig2, a.tau,
-                                  tl, a.sigma, a.shrink, queue, bar);
+  // tile free of image-border pixels (uniform per CTA): flag-free fast path
+  const bool interior = ox >= 1 && oy >= 1 && ox + TW <= W - 1 && oy + TH <= H - 1;
+#define FT_PD_CALL(P2_, IN_)                                                                  \
+  pd_iterate<TW, BY, PY, P2_, IN_>(a.iters, sm, base, tx, fl, u1, u2, gx, gy, r0, thr, ig2,   \
+                                   a.tau, tl, a.sigma, a.shrink, queue, bar)
+  if (a.pow2) {
+    if (interior) FT_PD_CALL(true, true); else FT_PD_CALL(true, false);
+  } else {
+    if (interior) FT_PD_CALL(false, true); else FT_PD_CALL(false, false);
+  }
+#undef FT_PD_CALL
 
   // ---- write back the exact interior
   const int lo_x = a.halo, hi_x = TW - a.halo;
@@ -803,7 +814,7 @@ __global__ void __launch_bounds__(32 * kCBY, 1) k_level_cluster(const LevelArgs 
     }
     xch.after_primal();  // publish u-bar edges before the first dual step
 
-    pd_iterate<kCTW, kCBY, kCPY, false>(a.iters, sm, base, tx, fl, u1, u2, gx, gy, r0, thr, ig2, a.tau,
+    pd_iterate<kCTW, kCBY, kCPY, false, false>(a.iters, sm, base, tx, fl, u1, u2, gx, gy, r0, thr, ig2, a.tau,
                                  tl, a.sigma, a.shrink, queue, xch);
 
     // ---- 3x3 median of u1, u2 with replicated borders (:210-211).  The p
@@ -992,11 +1003,11 @@ __global__ void __launch_bounds__(32 * BY, 1) k_pd_persist(const PDArgs a) {
 
     BlockBarrier bar;
     if (a.pow2)
-      pd_iterate<TW, BY, PY, true>(a.iters, sm, base, tx, fl, u1, u2, gx, gy, r0, thr, ig2,
-                                   a.tau, tl, a.sigma, a.shrink, queue, bar);
+      pd_iterate<TW, BY, PY, true, false>(a.iters, sm, base, tx, fl, u1, u2, gx, gy, r0, thr,
+                                          ig2, a.tau, tl, a.sigma, a.shrink, queue, bar);
     else
-      pd_iterate<TW, BY, PY, false>(a.iters, sm, base, tx, fl, u1, u2, gx, gy, r0, thr, ig2,
-                                    a.tau, tl, a.sigma, a.shrink, queue, bar);
+      pd_iterate<TW, BY, PY, false, false>(a.iters, sm, base, tx, fl, u1, u2, gx, gy, r0, thr,
+                                           ig2, a.tau, tl, a.sigma, a.shrink, queue, bar);
 
     // ---- write back the exact interior (drains during the next tile)
 #pragma unroll

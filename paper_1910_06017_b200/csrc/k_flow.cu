@@ -1119,8 +1119,8 @@ PDPlan pd_plan(int w, int h) {
     if (w <= c.tw && h <= c.th) return PDPlan{c, 0};
   }
   // defaults from the sweep on B200 (profiles/README.md): 32x32 tile,
-  // 512 threads, halo 3
-  return PDPlan{pd_config(env_int("FT_PD_CFG", 1)), env_int("FT_PD_HALO", 3)};
+  // 512 threads, halo 4
+  return PDPlan{pd_config(env_int("FT_PD_CFG", 1)), env_int("FT_PD_HALO", 4)};
 }
 
 // tau = 2^k (then sigma = 1/(8 tau) = 2^(-k-3) too): products by them are exact

@@ -173,6 +173,17 @@ int ft_tracker_step(ft_tracker *trk, const uint8_t *h_luma, int frame_index, con
  * host copy. */
 int ft_tracker_input_buffers(ft_tracker *trk, uint8_t **h_luma, ft_det **h_dets,
                              int32_t **h_n_dets);
+/* Asynchronous form of ft_tracker_step (the paper's
+ * prefetch / async-detection overlap).  Two pinned staging slots: stage
+ * frame t+1 into slot (t+1)&1 (ft_tracker_slot_buffers, or pass host
+ * pointers) and submit it while frame t is still running; wait returns a
+ * slot's records.  Submissions execute in order, so results are identical to
+ * the synchronous call.  NULL luma/dets/n_dets = already staged in the slot. */
+int ft_tracker_slot_buffers(ft_tracker *trk, int slot, uint8_t **h_luma, ft_det **h_dets,
+                            int32_t **h_n_dets);
+int ft_tracker_submit(ft_tracker *trk, int slot, int frame_index, const uint8_t *h_luma,
+                      const ft_det *h_dets, const int32_t *h_n_dets);
+int ft_tracker_wait(ft_tracker *trk, int slot, ft_track *h_out, int32_t *h_n_out);
 /* Same step with inputs already resident on the device (d_luma as above,
  * d_dets/d_n_dets device arrays); no host copies, no synchronisation. */
 int ft_tracker_step_device(ft_tracker *trk, const uint8_t *d_luma, int frame_index,

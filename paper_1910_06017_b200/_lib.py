@@ -91,6 +91,9 @@ SIGNATURES = {
     "ft_tracker_step": (_I, [_P, _P, _I, _P, _P, _P, _P]),
     "ft_tracker_input_buffers": (_I, [_P, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P)]),
     "ft_tracker_step_device": (_I, [_P, _P, _I, _P, _P]),
+    "ft_tracker_slot_buffers": (_I, [_P, _I, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P)]),
+    "ft_tracker_submit": (_I, [_P, _I, _I, _P, _P, _P]),
+    "ft_tracker_wait": (_I, [_P, _I, _P, _P]),
     "ft_tracker_read": (_I, [_P, _P, _P]),
     "ft_tracker_field": (_I, [_P, _I, C.POINTER(_P), C.POINTER(_P), C.POINTER(_I),
                               C.POINTER(_I)]),

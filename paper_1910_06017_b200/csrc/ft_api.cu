@@ -536,12 +536,31 @@ struct ft_tracker {
   int32_t *d_nout = nullptr;
   TrackerDev T{};
   FlowWork fw;
-  // pinned staging
+  // pinned staging, double-buffered: slot k holds the inputs / outputs of
+  // every submission with frame parity k so the host can stage frame t+1
+  // while the device runs frame t (ft_tracker_submit / ft_tracker_wait).
+  // h_* point at the slot being staged or read.
+  struct Slot {
+    uint8_t *luma = nullptr;
+    ft_det *dets = nullptr;
+    int32_t *in = nullptr;
+    ft_track *out = nullptr;
+    int32_t *nout = nullptr;
+    cudaEvent_t done = nullptr;
+    bool pending = false;
+  } slots[2];
   uint8_t *h_luma = nullptr;
   ft_det *h_dets = nullptr;
   int32_t *h_in = nullptr;
   ft_track *h_out = nullptr;
   int32_t *h_nout = nullptr;
+  void use_slot(int k) {
+    h_luma = slots[k].luma;
+    h_dets = slots[k].dets;
+    h_in = slots[k].in;
+    h_out = slots[k].out;
+    h_nout = slots[k].nout;
+  }
   // graphs keyed by (has_prev, input pointers)
   struct GraphKey {
     int has_prev;
@@ -641,8 +660,10 @@ struct ft_tracker {
       timer.report();
       return rc;
     }
-    GraphKey key{has_prev ? 1 : 0, host_io ? nullptr : luma, host_io ? nullptr : dets,
-                 host_io ? nullptr : in};
+    // host-I/O graphs bake the staging slot's pinned pointers into their
+    // copy nodes: key them by those pointers (one graph per slot)
+    GraphKey key{has_prev ? 1 : 0, host_io ? (const void *)h_luma : luma,
+                 host_io ? (const void *)h_dets : dets, host_io ? (const void *)h_in : in};
     auto it = graphs.find(key);
     if (it == graphs.end()) {
       Graph g;
@@ -677,6 +698,8 @@ struct ft_tracker {
 static int read_staged(ft_tracker *t, ft_track *out, int32_t *n_out);
 
 extern "C" {
+int ft_tracker_slot_buffers(ft_tracker *t, int slot, uint8_t **luma, ft_det **dets,
+                            int32_t **n_dets);
 
 int ft_tracker_create(ft_ctx *ctx, const ft_tracker_config *cfg, ft_tracker **out) {
   if (!ctx || !cfg || !out) return fail(FT_EINVAL, "NULL argument");
@@ -767,12 +790,16 @@ int ft_tracker_create(ft_ctx *ctx, const ft_tracker_config *cfg, ft_tracker **ou
   FT_TRY(t->alloc(&T.cost, (size_t)S * C * D));
   FT_TRY(t->alloc(&T.lost, (size_t)S * C));
   FT_TRY(tracker_kernel_setup(T));
-  // pinned staging
-  FT_CUDA_TRY(cudaMallocHost(&t->h_luma, (size_t)S * t->W * t->H));
-  FT_CUDA_TRY(cudaMallocHost(&t->h_dets, (size_t)S * D * sizeof(ft_det)));
-  FT_CUDA_TRY(cudaMallocHost(&t->h_in, (size_t)(S + 1) * 4));
-  FT_CUDA_TRY(cudaMallocHost(&t->h_out, (size_t)S * 2 * C * sizeof(ft_track)));
-  FT_CUDA_TRY(cudaMallocHost(&t->h_nout, (size_t)2 * S * 4));
+  // pinned staging, two slots
+  for (auto &sl : t->slots) {
+    FT_CUDA_TRY(cudaMallocHost(&sl.luma, (size_t)S * t->W * t->H));
+    FT_CUDA_TRY(cudaMallocHost(&sl.dets, (size_t)S * D * sizeof(ft_det)));
+    FT_CUDA_TRY(cudaMallocHost(&sl.in, (size_t)(S + 1) * 4));
+    FT_CUDA_TRY(cudaMallocHost(&sl.out, (size_t)S * 2 * C * sizeof(ft_track)));
+    FT_CUDA_TRY(cudaMallocHost(&sl.nout, (size_t)2 * S * 4));
+    FT_CUDA_TRY(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
+  }
+  t->use_slot(0);
   *out = t.release();
   return ft_tracker_reset(*out);
 }
@@ -800,11 +827,14 @@ int ft_tracker_destroy(ft_tracker *t) {
   for (auto &kv : t->graphs) cudaGraphExecDestroy(kv.second.exec);
   for (void *p : t->allocs) cudaFree(p);
   flow_work_free(t->fw);
-  cudaFreeHost(t->h_luma);
-  cudaFreeHost(t->h_dets);
-  cudaFreeHost(t->h_in);
-  cudaFreeHost(t->h_out);
-  cudaFreeHost(t->h_nout);
+  for (auto &sl : t->slots) {
+    cudaFreeHost(sl.luma);
+    cudaFreeHost(sl.dets);
+    cudaFreeHost(sl.in);
+    cudaFreeHost(sl.out);
+    cudaFreeHost(sl.nout);
+    if (sl.done) cudaEventDestroy(sl.done);
+  }
   if (t->ev_in) cudaEventDestroy(t->ev_in);
   if (t->ev_out) cudaEventDestroy(t->ev_out);
   if (t->stream) cudaStreamDestroy(t->stream);
@@ -813,30 +843,62 @@ int ft_tracker_destroy(ft_tracker *t) {
 }
 
 int ft_tracker_input_buffers(ft_tracker *t, uint8_t **luma, ft_det **dets, int32_t **n_dets) {
-  if (!t) return fail(FT_EINVAL, "tracker is NULL");
-  if (luma) *luma = t->h_luma;
-  if (dets) *dets = t->h_dets;
-  if (n_dets) *n_dets = t->h_in + 1;
+  return ft_tracker_slot_buffers(t, 0, luma, dets, n_dets);
+}
+
+int ft_tracker_slot_buffers(ft_tracker *t, int slot, uint8_t **luma, ft_det **dets,
+                            int32_t **n_dets) {
+  if (!t || slot < 0 || slot > 1) return fail(FT_EINVAL, "bad tracker / slot");
+  if (luma) *luma = t->slots[slot].luma;
+  if (dets) *dets = t->slots[slot].dets;
+  if (n_dets) *n_dets = t->slots[slot].in + 1;
   return FT_OK;
+}
+
+// Enqueue one step reading the inputs staged in `slot`; returns without
+// waiting.  Steps execute in submission order on the tracker's stream.
+int ft_tracker_submit(ft_tracker *t, int slot, int frame, const uint8_t *luma, const ft_det *dets,
+                      const int32_t *n_dets) {
+  if (!t || slot < 0 || slot > 1) return fail(FT_EINVAL, "bad tracker / slot");
+  auto &sl = t->slots[slot];
+  if (sl.pending) return fail(FT_EINVAL, "slot still in flight: call ft_tracker_wait first");
+  const int S = t->S, D = t->cfg.max_dets;
+  const int32_t *nd = n_dets ? n_dets : sl.in + 1;
+  for (int s = 0; s < S; ++s)
+    if (nd[s] > D) return fail(FT_ECAP, "more detections than max_dets");
+  DeviceGuard g(t->ctx->device);
+  // stage into the slot's pinned memory unless the caller wrote there directly
+  if (luma && luma != sl.luma) std::memcpy(sl.luma, luma, (size_t)S * t->W * t->H);
+  if (dets && dets != sl.dets) std::memcpy(sl.dets, dets, (size_t)S * D * sizeof(ft_det));
+  if (nd != sl.in + 1) std::memcpy(sl.in + 1, nd, (size_t)S * 4);
+  sl.in[0] = frame;
+  t->use_slot(slot);
+  FT_TRY(t->join_in());
+  FT_TRY(t->run(t->frames_seen > 0, nullptr, nullptr, nullptr, true));
+  FT_CUDA_TRY(cudaEventRecord(sl.done, t->stream));
+  FT_TRY(t->join_out());
+  sl.pending = true;
+  t->frames_seen++;
+  return FT_OK;
+}
+
+// Wait for the step submitted in `slot` and return its track records.
+int ft_tracker_wait(ft_tracker *t, int slot, ft_track *out, int32_t *n_out) {
+  if (!t || slot < 0 || slot > 1) return fail(FT_EINVAL, "bad tracker / slot");
+  auto &sl = t->slots[slot];
+  if (!sl.pending) return fail(FT_EINVAL, "nothing submitted in this slot");
+  DeviceGuard g(t->ctx->device);
+  FT_CUDA_TRY(cudaEventSynchronize(sl.done));
+  sl.pending = false;
+  t->use_slot(slot);
+  return read_staged(t, out, n_out);
 }
 
 int ft_tracker_step(ft_tracker *t, const uint8_t *luma, int frame, const ft_det *dets,
                     const int32_t *n_dets, ft_track *out, int32_t *n_out) {
   if (!t || !luma || !n_dets) return fail(FT_EINVAL, "NULL argument");
-  const int S = t->S, D = t->cfg.max_dets;
-  for (int s = 0; s < S; ++s)
-    if (n_dets[s] > D) return fail(FT_ECAP, "more detections than max_dets");
-  DeviceGuard g(t->ctx->device);
-  // stage into pinned memory unless the caller wrote there directly
-  if (luma != t->h_luma) std::memcpy(t->h_luma, luma, (size_t)S * t->W * t->H);
-  if (dets && dets != t->h_dets) std::memcpy(t->h_dets, dets, (size_t)S * D * sizeof(ft_det));
-  if (n_dets != t->h_in + 1) std::memcpy(t->h_in + 1, n_dets, (size_t)S * 4);
-  t->h_in[0] = frame;
-  FT_TRY(t->join_in());
-  FT_TRY(t->run(t->frames_seen > 0, nullptr, nullptr, nullptr, true));
-  FT_CUDA_TRY(cudaStreamSynchronize(t->stream));
-  t->frames_seen++;
-  return read_staged(t, out, n_out);
+  FT_TRY(ft_tracker_submit(t, 0, frame, luma, dets, n_dets));
+  return ft_tracker_wait(t, 0, out, n_out);
 }
 
 int ft_tracker_step_device(ft_tracker *t, const uint8_t *d_luma, int frame, const ft_det *d_dets,
@@ -865,6 +927,7 @@ int ft_tracker_read(ft_tracker *t, ft_track *out, int32_t *n_out) {
   DeviceGuard g(t->ctx->device);
   cudaStream_t s = t->stream;
   FT_TRY(t->join_in());
+  t->use_slot(0);
   FT_CUDA_TRY(cudaMemcpyAsync(t->h_out, t->d_out, (size_t)t->S * 2 * t->cfg.max_tracks * sizeof(ft_track),
                               cudaMemcpyDeviceToHost, s));
   FT_CUDA_TRY(cudaMemcpyAsync(t->h_nout, t->d_nout, (size_t)2 * t->S * 4, cudaMemcpyDeviceToHost, s));

@@ -52,18 +52,24 @@ class Tracker:
         h = C.c_void_p()
         _lib.check(self._lib.ft_tracker_create(self._ctx, C.byref(cfg), C.byref(h)))
         self._h = h.value
-        # pinned staging owned by the library, viewed as numpy
-        pl, pd, pn = C.c_void_p(), C.c_void_p(), C.c_void_p()
-        _lib.check(self._lib.ft_tracker_input_buffers(self._h, C.byref(pl), C.byref(pd),
-                                                      C.byref(pn)))
+        # pinned staging owned by the library (two slots), viewed as numpy
         S = self.n_streams
-        self.luma_in = np.ctypeslib.as_array(
-            (C.c_uint8 * (S * self.height * self.width)).from_address(pl.value)
-        ).reshape(S, self.height, self.width)
-        self.dets_in = np.frombuffer(
-            (C.c_uint8 * (S * self.max_dets * _lib.DET_DTYPE.itemsize)).from_address(pd.value),
-            dtype=_lib.DET_DTYPE).reshape(S, self.max_dets)
-        self.ndets_in = np.ctypeslib.as_array((C.c_int32 * S).from_address(pn.value))
+        self._slots = []
+        for slot in (0, 1):
+            pl, pd, pn = C.c_void_p(), C.c_void_p(), C.c_void_p()
+            _lib.check(self._lib.ft_tracker_slot_buffers(self._h, slot, C.byref(pl), C.byref(pd),
+                                                         C.byref(pn)))
+            luma = np.ctypeslib.as_array(
+                (C.c_uint8 * (S * self.height * self.width)).from_address(pl.value)
+            ).reshape(S, self.height, self.width)
+            dets = np.frombuffer(
+                (C.c_uint8 * (S * self.max_dets * _lib.DET_DTYPE.itemsize)).from_address(pd.value),
+                dtype=_lib.DET_DTYPE).reshape(S, self.max_dets)
+            nd = np.ctypeslib.as_array((C.c_int32 * S).from_address(pn.value))
+            self._slots.append((luma, dets, nd))
+        self.luma_in, self.dets_in, self.ndets_in = self._slots[0]
+        self._pending: list = []  # slots submitted and not yet waited, oldest first
+        self._next_slot = 0
         self._out = np.zeros((S, 2 * self.max_tracks), dtype=_lib.TRACK_DTYPE)
         self._nout = np.zeros(S, dtype=np.int32)
         self._labels: dict = {}
@@ -94,36 +100,37 @@ class Tracker:
             self._label_names.append(label)
         return ref
 
-    def _stage(self, frames, detections):
+    def _stage(self, frames, detections, slot: int = 0):
         S = self.n_streams
+        luma_in, dets_in, ndets_in = self._slots[slot]
         frames = np.asarray(frames, dtype=np.uint8)
         if frames.ndim == 2:
             frames = frames[None]
         if frames.shape != (S, self.height, self.width):
             raise ValueError(f"frames must be {(S, self.height, self.width)}, got {frames.shape}")
-        self.luma_in[...] = frames
+        luma_in[...] = frames
         if detections is None:
             detections = [None] * S
         if len(detections) != S:
             raise ValueError(f"need one detection list (or None) per stream ({S})")
         for s, dets in enumerate(detections):
             if dets is None:
-                self.ndets_in[s] = -1
+                ndets_in[s] = -1
                 continue
             if isinstance(dets, np.ndarray) and dets.dtype == _lib.DET_DTYPE:
                 n = len(dets)
                 if n > self.max_dets:
                     raise ValueError(f"{n} detections exceed max_dets={self.max_dets}")
-                self.dets_in[s, :n] = dets
-                self.ndets_in[s] = n
+                dets_in[s, :n] = dets
+                ndets_in[s] = n
                 continue
             n = len(dets)
             if n > self.max_dets:
                 raise ValueError(f"{n} detections exceed max_dets={self.max_dets}")
-            rec = self.dets_in[s]
+            rec = dets_in[s]
             for j, d in enumerate(dets):
                 rec[j] = (d.class_id, self._label_ref(d.label), d.score, *d.box)
-            self.ndets_in[s] = n
+            ndets_in[s] = n
 
     def step_records(self, frames, frame_index: int, detections=None):
         """One frame for every stream; returns a list (per stream) of
@@ -136,11 +143,34 @@ class Tracker:
         self._frame = frame_index
         return [self._out[s, :self._nout[s]] for s in range(self.n_streams)]
 
+    # ------------------------------------------------------------------ async
+    def submit(self, frames, frame_index: int, detections=None) -> None:
+        """Stage one frame per stream into the next pinned slot and enqueue
+        the step without waiting (at most two in flight).  Results come
+        back, in order, from `wait()`; they equal step_records' output."""
+        if len(self._pending) == 2:
+            raise RuntimeError("two steps in flight: call wait() first")
+        slot = self._next_slot
+        self._stage(frames, detections, slot)
+        _lib.check(self._lib.ft_tracker_submit(self._h, slot, int(frame_index), None, None, None))
+        self._pending.append(slot)
+        self._next_slot ^= 1
+
+    def wait(self):
+        """Records of the oldest submitted step (see step_records)."""
+        slot = self._pending.pop(0)
+        _lib.check(self._lib.ft_tracker_wait(self._h, slot, _lib.ptr(self._out),
+                                             _lib.ptr(self._nout)))
+        return [self._out[s, :self._nout[s]].copy() for s in range(self.n_streams)]
+
     def step(self, frames, frame_index: int, detections=None):
         """One frame for every stream; returns, per stream, the full scene
         list (SceneObjects, Lost tombstones included, id order) exactly like
         the reference's scene after `update`."""
-        recs = self.step_records(frames, frame_index, detections)
+        return self.scenes(self.step_records(frames, frame_index, detections))
+
+    def scenes(self, recs):
+        """Full scene lists from one step's records (keeps the tombstones)."""
         scenes = []
         for s, r in enumerate(recs):
             active, newly_lost = [], []
@@ -148,8 +178,7 @@ class Tracker:
                 obj = self._obj(row)
                 (active if obj.state == ACTIVE else newly_lost).append(obj)
             self._tombstones[s].extend(newly_lost)
-            scene = sorted(self._tombstones[s] + active, key=lambda o: o.id)
-            scenes.append(scene)
+            scenes.append(sorted(self._tombstones[s] + active, key=lambda o: o.id))
         return scenes
 
     def _obj(self, row) -> SceneObject:
@@ -232,17 +261,38 @@ def read_mot(fh) -> list:
     return rows
 
 
-def run(frames, source, width: int, height: int, detect_every: int = 1, **tracker_kw):
-    """Drive a single-stream Tracker over an iterable of u8 luma frames with
-    a DetectionSource.  Frames whose index is not a
-    multiple of `detect_every` have no detector result (coast).  Yields
-    (frame_index, scene) per frame."""
+def run(frames, source, width: int, height: int, detect_every: int = 1,
+        pipelined: bool = True, **tracker_kw):
+    """Drive a single-stream Tracker over an iterable of u8 luma frames (or
+    Frames) with a DetectionSource.  Frames whose index is
+    not a multiple of `detect_every` have no detector result (coast).
+    Yields (frame_index, scene) per frame, in order.
+
+    pipelined=True is the paper's concurrency:
+    frame t is submitted asynchronously, then the detector lookup and host
+    staging of frame t+1 run while the device processes frame t; results are
+    byte-identical to the sequential mode, emitted with one frame of lag."""
     trk = Tracker(width, height, n_streams=1, **tracker_kw)
+
+    def as_u8(luma):
+        if hasattr(luma, "data") and not isinstance(luma, np.ndarray):
+            return np.rint(np.asarray(luma.data) * 255.0).astype(np.uint8)
+        return luma
+
     try:
+        if not pipelined:
+            for t, luma in enumerate(frames):
+                dets = source.lookup(t) if t % detect_every == 0 else None
+                yield t, trk.step(as_u8(luma), t, [dets])[0]
+            return
+        last = None
         for t, luma in enumerate(frames):
-            if hasattr(luma, "data") and not isinstance(luma, np.ndarray):
-                luma = np.rint(np.asarray(luma.data) * 255.0).astype(np.uint8)
-            dets = source.lookup(t) if t % detect_every == 0 else None
-            yield t, trk.step(luma, t, [dets])[0]
+            dets = source.lookup(t) if t % detect_every == 0 else None  # overlaps frame t-1
+            trk.submit(as_u8(luma), t, [dets])
+            if last is not None:
+                yield last, trk.scenes(trk.wait())[0]
+            last = t
+        if last is not None:
+            yield last, trk.scenes(trk.wait())[0]
     finally:
         trk.close()

@@ -136,3 +136,27 @@ def test_run_driver_matches_oracle():
         od = None if t % 2 else [O.Det(d.class_id, d.label, d.score, d.box) for d in dets[t]]
         O.step(st, frames[t], t, od, prm)
         assert [(o.id, o.box, o.state) for o in scene] == [(o.id, o.box, o.state) for o in st.tracks]
+
+
+@pytest.mark.gpu
+def test_pipelined_mode_equivalence():
+    """SPEC acceptance criterion 8: the concurrent / prefetch mode yields
+    byte-identical scenes to the sequential mode; with a slow detector the
+    lookup of frame t+1 overlaps the device work of frame t."""
+    import time
+
+    from paper_1910_06017_b200.optflow import FlowParams
+    from paper_1910_06017_b200.pipeline import run
+    from paper_1910_06017_b200.synth import make_sequence
+    frames, dets = make_sequence(160, 120, 6, 8, seed=62, det_every=1, scale_change=True)
+    src = detect.DelayedSource(detect.ScriptedSource({t: d for t, d in enumerate(dets)}), 0.02)
+    prm = FlowParams(warps_per_level=2, iterations_per_warp=20)
+    outs, times = {}, {}
+    for mode in (False, True):
+        t0 = time.perf_counter()
+        outs[mode] = [(t, [(o.id, o.box, o.state, o.lost_at) for o in sc])
+                      for t, sc in run(frames, src, 160, 120, detect_every=3, pipelined=mode,
+                                       flow_params=prm)]
+        times[mode] = time.perf_counter() - t0
+    assert outs[True] == outs[False]
+    assert [t for t, _ in outs[True]] == list(range(8))

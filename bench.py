@@ -324,7 +324,9 @@ def run_ours(args, ws, rank, local):
                 "roofline": {"bound": "hbm", "kernel": "k_pd_tile (TV-L1 primal-dual, finest level)",
                              "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                              "frac": round(achieved / hbm, 4), "traffic": traffic,
-                             "bytes_per_launch": bpl.value, "ms_per_launch": round(msl.value, 5),
+                             "bytes_per_launch": bpl.value,
+                             "compulsory_bytes_per_launch": bpl.value / max(ipl.value, 1),
+                             "ms_per_launch": round(msl.value, 5),
                              "iters_per_launch": ipl.value,
                              "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650",
                              "step_roofline_frac": round(step_frac, 4),

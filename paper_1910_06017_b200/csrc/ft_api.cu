@@ -987,9 +987,12 @@ int ft_tracker_profile_pd(ft_tracker *t, int reps, double *ms_per_launch, double
                 t->cfg.flow.warps_per_level, t->cfg.flow.iterations_per_warp};
   int iters = 0;
   FT_TRY(profile_pd(t->fw, t->PW, t->PH, t->S, p, reps, t->stream, ms_per_launch, &iters));
-  // compulsory HBM bytes of one launch: read 11 planes (8 state + gx gy
-  // rho0) and write 8 state planes once per pixel
-  if (bytes_per_launch) *bytes_per_launch = 152.0 * (double)t->P * t->S;
+  // algorithmic bytes of one launch per SURVEY.md 8(d): 152 B per
+  // pixel-iteration (read 11 planes: 8 state + gx gy rho0; write 8 state
+  // planes) x the pixel-iterations the launch performs.  The launch itself
+  // moves only ~152 B per pixel (temporal blocking keeps the state on chip
+  // across its iterations); bench.py reports that as compulsory bytes.
+  if (bytes_per_launch) *bytes_per_launch = 152.0 * (double)t->P * t->S * iters;
   if (iters_per_launch) *iters_per_launch = iters;
   return FT_OK;
 }

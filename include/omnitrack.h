@@ -61,7 +61,9 @@ int ft_device_count(int *count);
 int ft_ctx_create(int device, ft_ctx **out);
 int ft_ctx_destroy(ft_ctx *ctx);
 /* bind to an existing cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream);
- * NULL selects the context's own non-blocking stream */
+ * taken verbatim like the CUDA runtime: NULL is the legacy default stream.
+ * A new context starts on its own non-blocking stream.  Trackers run on
+ * their own stream, joined to this one by events at every call. */
 int ft_ctx_set_stream(ft_ctx *ctx, void *cuda_stream);
 int ft_ctx_synchronize(ft_ctx *ctx);
 
@@ -95,6 +97,13 @@ int ft_compute_flow(ft_ctx *ctx, const double *d_prev, const double *d_curr, int
 int ft_flow_energy_terms(ft_ctx *ctx, const double *d_prev, const double *d_curr,
                          const double *d_dx, const double *d_dy, int w, int h,
                          double huber_epsilon, double *d_data, double *d_s1, double *d_s2);
+
+/* compute_flow with energy_trace (optflow.py:212-213): after every warp of
+ * the finest scale the flow_energy terms are written to d_energy_terms
+ * (warps_per_level x 3 x w*h doubles: data, s1, s2 per warp) */
+int ft_compute_flow_traced(ft_ctx *ctx, const double *d_prev, const double *d_curr, int w, int h,
+                           const ft_flow_params *params, double *d_dx, double *d_dy,
+                           double *d_energy_terms);
 
 /* ---- tracking (track.py / assoc.py) ------------------------------------- */
 /* predict (track.py:56-87).  h_boxes: n x (x,y,w,h); field (d_dx,d_dy) is

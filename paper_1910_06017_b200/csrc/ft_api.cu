@@ -286,6 +286,10 @@ int ft_structure_texture(ft_ctx *ctx, const double *in, int w, int h, double wei
                                   (double *)ctx->scratch, 0, 1, ctx->stream);
 }
 
+int ft_compute_flow_traced(ft_ctx *ctx, const double *prev, const double *curr, int w, int h,
+                           const ft_flow_params *params, double *dx, double *dy,
+                           double *d_energy_terms);
+
 int ft_rof_denoise(ft_ctx *ctx, const double *in, int w, int h, double weight, int iterations,
                    double step, double *out) {
   if (!ctx || !in || !out) return fail(FT_EINVAL, "NULL argument");
@@ -301,6 +305,12 @@ int ft_rof_denoise(ft_ctx *ctx, const double *in, int w, int h, double weight, i
 
 int ft_compute_flow(ft_ctx *ctx, const double *prev, const double *curr, int w, int h,
                     const ft_flow_params *params, double *dx, double *dy) {
+  return ft_compute_flow_traced(ctx, prev, curr, w, h, params, dx, dy, nullptr);
+}
+
+int ft_compute_flow_traced(ft_ctx *ctx, const double *prev, const double *curr, int w, int h,
+                           const ft_flow_params *params, double *dx, double *dy,
+                           double *d_energy_terms) {
   if (!ctx || !prev || !curr || !dx || !dy) return fail(FT_EINVAL, "NULL argument");
   FT_TRY(check_flow_params(params));
   if (w < 2 || h < 2) return fail(FT_EINVAL, "frames must be at least 2x2");
@@ -319,7 +329,7 @@ int ft_compute_flow(ft_ctx *ctx, const double *prev, const double *curr, int w, 
   FlowParamsD p{params->data_weight, params->time_step, params->huber_epsilon,
                 params->warps_per_level, params->iterations_per_warp};
   return run_flow(p0, p1, 0, geo.w.data(), geo.h.data(), geo.off.data(), scales, p, ctx->fw, dx,
-                  dy, 0, 1, ctx->stream);
+                  dy, 0, 1, ctx->stream, d_energy_terms);
 }
 
 int ft_flow_energy_terms(ft_ctx *ctx, const double *prev, const double *curr, const double *dx,

@@ -158,7 +158,8 @@ struct FlowParamsD {
 // Result flow at level 0 written to (dx, dy) with stride out_stride.
 int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const int *lw,
              const int *lh, const int64_t *loff, int scales, const FlowParamsD &p, FlowWork &fw,
-             double *dx, double *dy, int64_t out_stride, int nb, cudaStream_t s);
+             double *dx, double *dy, int64_t out_stride, int nb, cudaStream_t s,
+             double *energy_terms = nullptr);
 
 int launch_energy_terms(const double *i0, const double *i1, const double *u1, const double *u2,
                         int w, int h, double eps, double *data, double *s1, double *s2,

@@ -1274,7 +1274,8 @@ void flow_work_free(FlowWork &fw) {
 
 int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const int *lw,
              const int *lh, const int64_t *loff, int scales, const FlowParamsD &p, FlowWork &fw,
-             double *dx, double *dy, int64_t out_stride, int nb, cudaStream_t s) {
+             double *dx, double *dy, int64_t out_stride, int nb, cudaStream_t s,
+             double *energy_terms) {
   const int64_t cap = fw.cap;
   if (nb > fw.nb || (int64_t)lw[0] * lh[0] > cap) return fail(FT_EINVAL, "flow workspace too small");
   int cur = 0;
@@ -1382,6 +1383,13 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
                                                 cap);
       count_launch();
       cur = 1 - cur;
+      if (energy_terms && lvl == 0 && nb == 1) {  // energy_trace (optflow.py:212-213)
+        const int64_t n0 = (int64_t)w * h;
+        StatePtrs now = state_ptrs(fw.st[cur], fw.nb, cap);
+        double *tb = energy_terms + (int64_t)wp * 3 * n0;
+        FT_TRY(launch_energy_terms(i0, i1, now.p[U1], now.p[U2], w, h, p.eps, tb, tb + n0,
+                                   tb + 2 * n0, s));
+      }
     }
     phase_mark(kLevelNames[lvl < 8 ? lvl : 7]);
   }

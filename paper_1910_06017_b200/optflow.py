@@ -177,14 +177,13 @@ def compute_flow(prev: Frame, curr: Frame, params: FlowParams = FlowParams(),
                  energy_trace: list | None = None) -> MotionField:
     """Coarse-to-fine TV-L1 from prev to curr (optflow.py:217-253).
 
-    Both frames are expected to be structure-texture preprocessed.
-    `energy_trace` (a diagnostic) is not supported
-    on the device path.
+    Both frames are expected to be structure-texture preprocessed.  When
+    `energy_trace` is a list, the finest-scale objective after every warp is
+    appended to it (optflow.py:212-213): the device writes the per-pixel
+    terms after each warp and they are summed in numpy's order here.
     """
     import torch
 
-    if energy_trace is not None:
-        raise NotImplementedError("energy_trace is a CPU diagnostic, not part of the device path")
     if (prev.width, prev.height) != (curr.width, curr.height):
         raise ValueError(f"frame sizes differ: {prev.width}x{prev.height} vs "
                          f"{curr.width}x{curr.height}")
@@ -195,7 +194,20 @@ def compute_flow(prev: Frame, curr: Frame, params: FlowParams = FlowParams(),
     dx = torch.empty_like(a)
     dy = torch.empty_like(a)
     prm = _lib.flow_params_struct(params)
-    _lib.check(_lib.load().ft_compute_flow(_lib.ctx(), _lib.ptr(a), _lib.ptr(b), prev.width,
-                                           prev.height, C.byref(prm), _lib.ptr(dx),
-                                           _lib.ptr(dy)))
+    if energy_trace is None:
+        _lib.check(_lib.load().ft_compute_flow(_lib.ctx(), _lib.ptr(a), _lib.ptr(b), prev.width,
+                                               prev.height, C.byref(prm), _lib.ptr(dx),
+                                               _lib.ptr(dy)))
+    else:
+        n = prev.width * prev.height
+        terms = torch.empty((params.warps_per_level, 3, n), dtype=torch.float64, device=a.device)
+        _lib.check(_lib.load().ft_compute_flow_traced(
+            _lib.ctx(), _lib.ptr(a), _lib.ptr(b), prev.width, prev.height, C.byref(prm),
+            _lib.ptr(dx), _lib.ptr(dy), _lib.ptr(terms)))
+        host = terms.cpu().numpy().reshape(params.warps_per_level, 3, prev.height, prev.width)
+        for data, s1, s2 in host:  # _energy (optflow.py:127-137) summed like numpy
+            total = params.data_weight * float(np.abs(data).sum())
+            total += float(s1.sum())
+            total += float(s2.sum())
+            energy_trace.append(total)
     return MotionField(prev.width, prev.height, dx, dy, frame_index=curr.index)

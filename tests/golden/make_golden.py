@@ -291,6 +291,9 @@ def gen_io():
         fld = optflow.MotionField(width=pa.width, height=pa.height, dx=z["f0_dx"], dy=z["f0_dy"])
         out["energy"] = np.array([optflow.flow_energy(pa, pb, fld),
                                   optflow.flow_energy(pa, pb, fld, optflow.FlowParams(huber_epsilon=0.0))])
+        trace = []
+        optflow.compute_flow(pa, pb, optflow.FlowParams(), energy_trace=trace)
+        out["energy_trace"] = np.array(trace)
         optflow.write_flo(fld, os.path.join(d, "f.flo"))
         out["flo_bytes"] = np.frombuffer(open(os.path.join(d, "f.flo"), "rb").read(), np.uint8)
     save("io.npz", **out)

@@ -160,3 +160,15 @@ def test_pipelined_mode_equivalence():
         times[mode] = time.perf_counter() - t0
     assert outs[True] == outs[False]
     assert [t for t, _ in outs[True]] == list(range(8))
+
+
+@pytest.mark.gpu
+def test_energy_trace_matches_reference(golden):
+    from paper_1910_06017_b200.imaging import Frame
+    from paper_1910_06017_b200.optflow import compute_flow
+    zf, zi = golden("flow.npz"), golden("io.npz")
+    a, b = Frame.from_array(zf["f0_sta"]), Frame.from_array(zf["f0_stb"], 1)
+    trace = []
+    fld = compute_flow(a, b, energy_trace=trace)
+    assert np.array_equal(np.array(trace), zi["energy_trace"])
+    assert np.array_equal(fld.dx, zf["f0_dx"])

@@ -111,6 +111,14 @@ int ft_compute_flow_traced(ft_ctx *ctx, const double *d_prev, const double *d_cu
 int ft_predict(ft_ctx *ctx, const double *h_boxes, int n, const double *d_dx, const double *d_dy,
                int field_w, int field_h, int level, int frame_w, int frame_h, double *h_out,
                uint8_t *h_valid);
+/* KLT / MedianFlow box prediction (oracle/klt_oracle.py
+ * defines it -- the reference has no KLT): prev/curr are the w x h
+ * processing-level frames of pyramid `level`; grid x grid points per box,
+ * pyramidal LK prev->curr and back, forward-backward median filter, median
+ * shift and pairwise scale ratio.  h_valid[i]=0 when no point survives. */
+int ft_klt_predict(ft_ctx *ctx, const double *d_prev, const double *d_curr, int w, int h,
+                   int level, int frame_w, int frame_h, int grid, const double *h_boxes, int n,
+                   double *h_out, uint8_t *h_valid);
 /* iou (assoc.py:30-41) matrix: h_out[i*n+j] = iou(a_i, b_j) */
 int ft_iou_matrix(ft_ctx *ctx, const double *h_a, int m, const double *h_b, int n, double *h_out);
 /* hungarian (assoc.py:84-106): h_cost m x n; pairs sorted by row;

@@ -84,6 +84,7 @@ SIGNATURES = {
     "ft_compute_flow": (_I, [_P, _P, _P, _I, _I, C.POINTER(ft_flow_params), _P, _P]),
     "ft_compute_flow_traced": (_I, [_P, _P, _P, _I, _I, C.POINTER(ft_flow_params), _P, _P, _P]),
     "ft_predict": (_I, [_P, _P, _I, _P, _P, _I, _I, _I, _I, _I, _P, _P]),
+    "ft_klt_predict": (_I, [_P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _I, _P, _P]),
     "ft_iou_matrix": (_I, [_P, _P, _I, _P, _I, _P]),
     "ft_hungarian": (_I, [_P, _P, _I, _I, _I, _D, _P, C.POINTER(_I)]),
     "ft_match": (_I, [_P, _P, _P, _I, _P, _P, _I, _D, _P, _P, C.POINTER(_I)]),

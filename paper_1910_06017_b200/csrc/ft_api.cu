@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "ft_internal.cuh"
+#include "ft_klt.cuh"
 #include "ft_tracker.cuh"
 
 namespace ft {
@@ -346,6 +347,69 @@ int ft_flow_energy_terms(ft_ctx *ctx, const double *prev, const double *curr, co
   FT_TRY(launch_scale_copy(prev, n, 0, i0, 0, 255.0, 1, ctx->stream));
   FT_TRY(launch_scale_copy(curr, n, 0, i1, 0, 255.0, 1, ctx->stream));
   return launch_energy_terms(i0, i1, dx, dy, w, h, huber_epsilon, data, s1, s2, ctx->stream);
+}
+
+static int check_boxes(const double *b, int n);
+
+// Build one frame's KLT pyramid (levels + central gradients) into `buf`
+// (3 x geo.total doubles per image) from the processing-level frame.
+static int build_klt_pyramid(const double *img, int64_t img_stride, const Geometry &geo,
+                             double *buf, int64_t stride, int nb, cudaStream_t s, KltPyr &out) {
+  double *lvl = buf, *gx = buf + geo.total, *gy = buf + 2 * geo.total;
+  for (int b = 0; b < nb; ++b)
+    FT_CUDA_TRY(cudaMemcpyAsync(lvl + b * stride, img + b * img_stride,
+                                (size_t)geo.w[0] * geo.h[0] * 8, cudaMemcpyDeviceToDevice, s));
+  for (int l = 1; l < geo.n; ++l)
+    FT_TRY(launch_blur_decimate(lvl + geo.off[l - 1], geo.w[l - 1], geo.h[l - 1], stride,
+                                lvl + geo.off[l], stride, nullptr, 0, 1.0, nb, s));
+  for (int l = 0; l < geo.n; ++l)
+    FT_TRY(launch_central_grad(lvl + geo.off[l], geo.w[l], geo.h[l], stride, gx + geo.off[l],
+                               gy + geo.off[l], stride, nb, s));
+  out.lvl = lvl;
+  out.gx = gx;
+  out.gy = gy;
+  out.stride = stride;
+  for (int l = 0; l < kKltLevels; ++l) {
+    out.w[l] = geo.w[l];
+    out.h[l] = geo.h[l];
+    out.off[l] = geo.off[l];
+  }
+  return FT_OK;
+}
+
+int ft_klt_predict(ft_ctx *ctx, const double *prev, const double *curr, int w, int h, int level,
+                   int frame_w, int frame_h, int grid, const double *h_boxes, int n,
+                   double *h_out, uint8_t *h_valid) {
+  if (!ctx || !prev || !curr || (n > 0 && (!h_boxes || !h_out || !h_valid)))
+    return fail(FT_EINVAL, "NULL argument");
+  if (grid < 1 || grid > 11) return fail(FT_EINVAL, "grid must be in 1..11");
+  FT_TRY(check_pyramid(w, h, kKltLevels));
+  if (n <= 0) return FT_OK;
+  FT_TRY(check_boxes(h_boxes, n));
+  DeviceGuard g(ctx->device);
+  Geometry geo;
+  geo.build(w, h, kKltLevels);
+  const int gg = grid * grid;
+  const size_t need = (size_t)6 * geo.total + (size_t)n * (8 + 5 * gg) + n + 64;
+  FT_TRY(ctx->ensure_scratch(need * 8));
+  double *pa = (double *)ctx->scratch, *pb = pa + 3 * geo.total;
+  double *boxes = pb + 3 * geo.total, *out = boxes + 4 * n;
+  double *pts = out + 4 * n, *fwd = pts + 2 * (size_t)n * gg, *fb = fwd + 2 * (size_t)n * gg;
+  unsigned char *valid = (unsigned char *)(fb + (size_t)n * gg);
+  cudaStream_t s = ctx->stream;
+  KltArgs a;
+  FT_TRY(build_klt_pyramid(prev, 0, geo, pa, 0, 1, s, a.prev));
+  FT_TRY(build_klt_pyramid(curr, 0, geo, pb, 0, 1, s, a.curr));
+  a.grid = grid;
+  a.max_pts = gg;
+  a.scale = (double)(1 << level);
+  FT_CUDA_TRY(cudaMemcpyAsync(boxes, h_boxes, (size_t)n * 32, cudaMemcpyHostToDevice, s));
+  FT_TRY(launch_klt_predict(a, boxes, out, n, nullptr, n, 1, n, pts, fwd, fb, valid, frame_w,
+                            frame_h, s));
+  FT_CUDA_TRY(cudaMemcpyAsync(h_out, out, (size_t)n * 32, cudaMemcpyDeviceToHost, s));
+  FT_CUDA_TRY(cudaMemcpyAsync(h_valid, valid, (size_t)n, cudaMemcpyDeviceToHost, s));
+  FT_CUDA_TRY(cudaStreamSynchronize(s));
+  return FT_OK;
 }
 
 int ft_predict(ft_ctx *ctx, const double *h_boxes, int n, const double *dx, const double *dy,

@@ -68,6 +68,24 @@ __device__ __forceinline__ double glibc_hypot(double x, double y) {
   return glibc_hypot_kernel(ax, ay);
 }
 
+// bilinear_sample (imageops.py:53-66) at one point, clamped to the border:
+// np.clip(x, 0, w-1) = min(max(x, 0), w-1) with numpy's comparisons
+__device__ __forceinline__ double ft_bsample(const double *__restrict__ img, int w, int h,
+                                             double x, double y) {
+  x = x > 0.0 ? x : 0.0;
+  x = x < w - 1.0 ? x : w - 1.0;
+  y = y > 0.0 ? y : 0.0;
+  y = y < h - 1.0 ? y : h - 1.0;
+  const int x0 = (int)floor(x), y0 = (int)floor(y);
+  const int x1 = min(x0 + 1, w - 1), y1 = min(y0 + 1, h - 1);
+  const double fx = x - (double)x0, fy = y - (double)y0;
+  const double *r0 = img + (int64_t)y0 * w;
+  const double *r1 = img + (int64_t)y1 * w;
+  const double top = r0[x0] * (1.0 - fx) + r0[x1] * fx;
+  const double bot = r1[x0] * (1.0 - fx) + r1[x1] * fx;
+  return top * (1.0 - fy) + bot * fy;
+}
+
 // numpy maximum/minimum without NaNs: first argument wins ties
 __device__ __forceinline__ double np_max(double a, double b) { return a >= b ? a : b; }
 __device__ __forceinline__ double np_min(double a, double b) { return a <= b ? a : b; }

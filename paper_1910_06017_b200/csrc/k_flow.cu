@@ -1418,3 +1418,13 @@ int launch_energy_terms(const double *i0, const double *i1, const double *u1, co
   return FT_OK;
 }
 }  // namespace ft
+
+namespace ft {
+int launch_central_grad(const double *img, int w, int h, int64_t is, double *gx, double *gy,
+                        int64_t gs, int nb, cudaStream_t s) {
+  k_central_grad<<<grid2d(w, h, nb), dim3(32, 8), 0, s>>>(img, w, h, is, gx, gy, gs);
+  count_launch();
+  FT_CUDA_TRY(cudaGetLastError());
+  return FT_OK;
+}
+}  // namespace ft

@@ -1,0 +1,285 @@
+// KLT / MedianFlow motion backend (north_star items
+// (2)-(3)): pyramidal Lucas-Kanade on a GxG point grid per box, one warp per
+// point, window sums reduced with warp shuffles, forward-backward check,
+// median displacement and scale ratio per box.  The reference has no such
+// code; oracle/klt_oracle.py defines the algorithm and this file reproduces
+// it bit for bit (same IEEE operation order, same reduction tree).
+#include "ft_internal.cuh"
+#include "ft_klt.cuh"
+
+namespace ft {
+
+namespace {
+
+constexpr int kR = kKltR, kWin = (2 * kR + 1) * (2 * kR + 1);  // 81 window samples
+constexpr int kPerLane = (kWin + 31) / 32;                      // 3
+
+// lane-strided partial sum then xor butterfly (oracle: klt_oracle.lane_sum)
+__device__ __forceinline__ double warp_sum(double part) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) part = part + __shfl_xor_sync(0xffffffffu, part, off);
+  return part;
+}
+
+// Pyramidal LK of one point from pyramid A to pyramid B (image `img`);
+// identical on every lane of the warp.  Returns false when the point is lost.
+__device__ bool lk_point(const KltPyr &A, const KltPyr &B, int img, double px, double py,
+                         double &qx, double &qy) {
+  const int lane = threadIdx.x & 31;
+  double ga = 0.0, gb = 0.0;
+  bool ok = true;
+  for (int lvl = kKltLevels - 1; lvl >= 0; --lvl) {
+    const int w = A.w[lvl], h = A.h[lvl];
+    const int64_t o = (int64_t)img * A.stride + A.off[lvl];
+    const double *I = A.lvl + o, *Ix = A.gx + o, *Iy = A.gy + o;
+    const double *J = B.lvl + (int64_t)img * B.stride + B.off[lvl];
+    const double sc = (double)(1 << lvl);
+    const double cx = px / sc, cy = py / sc;
+    if (!(0.0 <= cx && cx <= w - 1.0 && 0.0 <= cy && cy <= h - 1.0)) {
+      ok = false;
+      break;
+    }
+    double ix[kPerLane], iy[kPerLane], iv[kPerLane];
+    double pxx = 0.0, pxy = 0.0, pyy = 0.0;
+#pragma unroll
+    for (int k = 0; k < kPerLane; ++k) {
+      const int e = lane + 32 * k;
+      ix[k] = iy[k] = iv[k] = 0.0;
+      if (e < kWin) {
+        const double wx = cx + (double)(e % (2 * kR + 1) - kR);
+        const double wy = cy + (double)(e / (2 * kR + 1) - kR);
+        ix[k] = ft_bsample(Ix, w, h, wx, wy);
+        iy[k] = ft_bsample(Iy, w, h, wx, wy);
+        iv[k] = ft_bsample(I, w, h, wx, wy);
+        pxx = pxx + ix[k] * ix[k];
+        pxy = pxy + ix[k] * iy[k];
+        pyy = pyy + iy[k] * iy[k];
+      }
+    }
+    const double gxx = warp_sum(pxx), gxy = warp_sum(pxy), gyy = warp_sum(pyy);
+    const double det = gxx * gyy - gxy * gxy;
+    if (!(det >= kKltMinDet)) {
+      ok = false;
+      break;
+    }
+    double vx = 0.0, vy = 0.0;
+    for (int it = 0; it < kKltIters; ++it) {
+      const double qx_ = cx + ga + vx, qy_ = cy + gb + vy;
+      double bxp = 0.0, byp = 0.0;
+#pragma unroll
+      for (int k = 0; k < kPerLane; ++k) {
+        const int e = lane + 32 * k;
+        if (e < kWin) {
+          const double jv = ft_bsample(J, w, h, qx_ + (double)(e % (2 * kR + 1) - kR),
+                                       qy_ + (double)(e / (2 * kR + 1) - kR));
+          const double dI = iv[k] - jv;
+          bxp = bxp + dI * ix[k];
+          byp = byp + dI * iy[k];
+        }
+      }
+      const double bx = warp_sum(bxp), by = warp_sum(byp);
+      const double ex = (gyy * bx - gxy * by) / det;
+      const double ey = (gxx * by - gxy * bx) / det;
+      vx = vx + ex;
+      vy = vy + ey;
+      if (ex * ex + ey * ey < kKltEps * kKltEps) break;
+    }
+    if (lvl > 0) {
+      ga = 2.0 * (ga + vx);
+      gb = 2.0 * (gb + vy);
+    } else {
+      ga = ga + vx;
+      gb = gb + vy;
+    }
+  }
+  qx = px + ga;
+  qy = py + gb;
+  if (ok && !(0.0 <= qx && qx <= B.w[0] - 1.0 && 0.0 <= qy && qy <= B.h[0] - 1.0)) ok = false;
+  return ok;
+}
+
+constexpr int kPtWarps = 8;
+
+// one warp per (stream, box, point): forward LK, then backward LK from the
+// forward result; writes the grid point, its forward position and the
+// forward-backward error (-1 when lost either way)
+__global__ void __launch_bounds__(32 * kPtWarps)
+    k_klt_points(KltArgs a, const double *boxes, int64_t box_stride, const int32_t *n_boxes,
+                 int n_boxes_const, double *pts, double *fwd, double *fb) {
+  const int s = blockIdx.y;
+  const int warp = threadIdx.x >> 5;
+  const int item = blockIdx.x * kPtWarps + warp;
+  const int G = a.grid, GG = G * G;
+  const int nb = n_boxes ? n_boxes[s] : n_boxes_const;
+  const int b = item / GG, k = item % GG;
+  if (b >= nb) return;
+  const double *box = boxes + ((int64_t)s * box_stride + b) * 4;
+  const double sc = a.scale;
+  const int i = k % G, j = k / G;
+  // x/s + (i+0.5)*(w/s)/G  (oracle order)
+  const double px = box[0] / sc + ((double)i + 0.5) * (box[2] / sc) / (double)G;
+  const double py = box[1] / sc + ((double)j + 0.5) * (box[3] / sc) / (double)G;
+  double qx, qy, rx, ry;
+  bool ok = lk_point(a.prev, a.curr, s, px, py, qx, qy);
+  if (ok) ok = lk_point(a.curr, a.prev, s, qx, qy, rx, ry);
+  if ((threadIdx.x & 31) == 0) {
+    const int64_t o = ((int64_t)s * box_stride + b) * a.max_pts + k;
+    pts[2 * o] = px;
+    pts[2 * o + 1] = py;
+    fwd[2 * o] = qx;
+    fwd[2 * o + 1] = qy;
+    fb[o] = ok ? glibc_hypot(rx - px, ry - py) : -1.0;
+  }
+}
+
+// warp bitonic sort of 128 doubles in shared memory (ascending)
+__device__ void warp_sort128(double *v) {
+  const int lane = threadIdx.x & 31;
+  for (int size = 2; size <= 128; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int t = lane + 32 * q;  // 64 compare-exchange pairs, 2 per lane
+        if (t < 64) {
+          const int lo = 2 * stride * (t / stride) + (t % stride);
+          const int hi = lo + stride;
+          const bool up = ((lo & size) == 0);
+          const double x = v[lo], y = v[hi];
+          if ((x > y) == up) {
+            v[lo] = y;
+            v[hi] = x;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+__device__ __forceinline__ double py_max2(double a, double b) { return b > a ? b : a; }
+__device__ __forceinline__ double py_min2(double a, double b) { return b < a ? b : a; }
+
+struct BoxScratch {
+  double v[128];
+  int kept[128];
+};
+
+// one warp per box: FB-median filter, median shift, pairwise scale ratio,
+// new box (klt_oracle.klt_predict steps 4-6).  valid[b] = 0 for None.
+__global__ void __launch_bounds__(32 * kPtWarps)
+    k_klt_boxes(KltArgs a, const double *boxes, double *out_boxes, int64_t box_stride,
+                const int32_t *n_boxes, int n_boxes_const, const double *pts, const double *fwd,
+                const double *fb, unsigned char *valid, int frame_w, int frame_h) {
+  __shared__ BoxScratch scr[kPtWarps];
+  const int s = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.x * kPtWarps + warp;
+  const int nb = n_boxes ? n_boxes[s] : n_boxes_const;
+  if (b >= nb) return;
+  BoxScratch &S = scr[warp];
+  const int GG = a.grid * a.grid;
+  const int64_t base = ((int64_t)s * box_stride + b) * a.max_pts;
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  // ---- lower median of the valid FB errors
+  int cnt = 0;
+  for (int k = lane; k < 128; k += 32) {
+    const double e = k < GG ? fb[base + k] : -1.0;
+    S.v[k] = e >= 0.0 ? e : inf;
+    cnt += e >= 0.0 ? 1 : 0;
+  }
+  const int nvalid = __reduce_add_sync(0xffffffffu, cnt);
+  __syncwarp();
+  const int64_t ob = ((int64_t)s * box_stride + b) * 4;
+  if (nvalid == 0) {
+    if (lane == 0) valid[(int64_t)s * box_stride + b] = 0;
+    return;
+  }
+  warp_sort128(S.v);
+  const double thr = S.v[(nvalid - 1) / 2];
+  __syncwarp();
+  // ---- kept points in point order (fb valid and <= thr)
+  int K = 0;
+  for (int k0 = 0; k0 < GG; k0 += 32) {
+    const int k = k0 + lane;
+    const double e = k < GG ? fb[base + k] : -1.0;
+    const bool keep = k < GG && e >= 0.0 && e <= thr;
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (keep) S.kept[K + __popc(m & ((1u << lane) - 1u))] = k;
+    K += __popc(m);
+  }
+  __syncwarp();
+  // ---- lower medians of kept dx and dy
+  double med[2];
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    for (int t = lane; t < 128; t += 32)
+      S.v[t] = t < K ? fwd[2 * (base + S.kept[t]) + c] - pts[2 * (base + S.kept[t]) + c] : inf;
+    __syncwarp();
+    warp_sort128(S.v);
+    med[c] = S.v[(K - 1) / 2];
+    __syncwarp();
+  }
+  // ---- scale: lower median of |p'_a - p'_b| / |p_a - p_b|, b = a + K/2
+  double scale = 1.0;
+  if (K >= 2) {
+    const int half = K / 2, npair = K - half;
+    int nr = 0;
+    for (int a0 = 0; a0 < npair; a0 += 32) {
+      const int aa = a0 + lane;
+      double r = 0.0;
+      bool has = false;
+      if (aa < npair) {
+        const int64_t ka = base + S.kept[aa], kb = base + S.kept[aa + half];
+        const double d0 = glibc_hypot(pts[2 * kb] - pts[2 * ka], pts[2 * kb + 1] - pts[2 * ka + 1]);
+        const double d1 = glibc_hypot(fwd[2 * kb] - fwd[2 * ka], fwd[2 * kb + 1] - fwd[2 * ka + 1]);
+        has = d0 > 0.0;
+        if (has) r = d1 / d0;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, has);
+      __syncwarp();
+      if (has) S.v[nr + __popc(m & ((1u << lane) - 1u))] = r;
+      nr += __popc(m);
+    }
+    __syncwarp();
+    if (nr > 0) {
+      for (int t = nr + lane; t < 128; t += 32) S.v[t] = inf;
+      __syncwarp();
+      warp_sort128(S.v);
+      scale = S.v[(nr - 1) / 2];
+    }
+  }
+  if (lane == 0) {
+    const double *bx = boxes + ob;
+    const double x = bx[0], y = bx[1], w = bx[2], h = bx[3];
+    const double sc = a.scale;
+    const double nw = w * scale, nh = h * scale;
+    const double cx = x + 0.5 * w + med[0] * sc;
+    const double cy = y + 0.5 * h + med[1] * sc;
+    out_boxes[ob] = py_min2(py_max2(cx - 0.5 * nw, 0.0), py_max2((double)frame_w - nw, 0.0));
+    out_boxes[ob + 1] = py_min2(py_max2(cy - 0.5 * nh, 0.0), py_max2((double)frame_h - nh, 0.0));
+    out_boxes[ob + 2] = nw;
+    out_boxes[ob + 3] = nh;
+    valid[(int64_t)s * box_stride + b] = 1;
+  }
+}
+
+}  // namespace
+
+int launch_klt_predict(const KltArgs &a, const double *boxes, double *out_boxes,
+                       int64_t box_stride, const int32_t *n_boxes, int n_boxes_const,
+                       int n_streams, int max_boxes, double *pts, double *fwd, double *fb,
+                       unsigned char *valid, int frame_w, int frame_h, cudaStream_t s) {
+  if (a.grid < 1 || a.grid * a.grid > 128) return fail(FT_EINVAL, "klt grid must be 1..11");
+  const int items = max_boxes * a.grid * a.grid;
+  if (items == 0) return FT_OK;
+  k_klt_points<<<dim3((items + kPtWarps - 1) / kPtWarps, n_streams), 32 * kPtWarps, 0, s>>>(
+      a, boxes, box_stride, n_boxes, n_boxes_const, pts, fwd, fb);
+  k_klt_boxes<<<dim3((max_boxes + kPtWarps - 1) / kPtWarps, n_streams), 32 * kPtWarps, 0, s>>>(
+      a, boxes, out_boxes, box_stride, n_boxes, n_boxes_const, pts, fwd, fb, valid, frame_w,
+      frame_h);
+  count_launch(2);
+  FT_CUDA_TRY(cudaGetLastError());
+  return FT_OK;
+}
+
+}  // namespace ft

@@ -150,3 +150,29 @@ def update(objects, assignment, detections, frame_index: int,
         else:
             out.append(rec)
     return out
+
+
+def predict_klt(objects, prev, curr, level: int, frame_size, grid: int = 10) -> list:
+    """KLT / MedianFlow alternative to `predict` (the
+    backend north_star describes, defined by oracle/klt_oracle.py since the
+    reference has none): a grid x grid point set per box is tracked with
+    pyramidal Lucas-Kanade between the processing-level frames `prev` and
+    `curr` (Frames, e.g. build_pyramid(f, L+1).levels[L]) and back, points
+    failing the forward-backward median test are dropped, and the box moves
+    by the median displacement and scales by the median pairwise distance
+    ratio.  Returns (x, y, w, h) or None per object, like `predict`."""
+    records = list(objects)
+    lost = next((r for r in records if r.state != ACTIVE), None)
+    if lost is not None:
+        raise ValueError(f"cannot predict lost object {lost.id}")
+    if not records:
+        return []
+    width, height = frame_size
+    src = _box_array(records)
+    dst = np.empty_like(src)
+    ok = np.empty(len(records), dtype=np.uint8)
+    a, b = prev.device(), curr.device()
+    _lib.check(_lib.load().ft_klt_predict(
+        _lib.ctx(), _lib.ptr(a), _lib.ptr(b), prev.width, prev.height, int(level), int(width),
+        int(height), int(grid), _lib.ptr(src), len(records), _lib.ptr(dst), _lib.ptr(ok)))
+    return [tuple(map(float, dst[k])) if ok[k] else None for k in range(len(records))]

@@ -173,7 +173,12 @@ typedef struct ft_tracker_config {
   double rof_weight;      /* 12.0 (imaging.py:128) */
   double rof_blend;       /* 0.05 */
   ft_flow_params flow;
+  int32_t motion;   /* FT_MOTION_TVL1 (reference path) or FT_MOTION_KLT */
+  int32_t klt_grid; /* KLT points per box side (1..11), default 10 */
 } ft_tracker_config;
+
+#define FT_MOTION_TVL1 0
+#define FT_MOTION_KLT 1
 
 int ft_tracker_create(ft_ctx *ctx, const ft_tracker_config *cfg, ft_tracker **out);
 int ft_tracker_destroy(ft_tracker *trk);

@@ -178,3 +178,34 @@ def klt_predict(boxes, prev: np.ndarray, curr: np.ndarray, level: int, frame_wh,
         ny = min(max(cy - 0.5 * nh, 0.0), max(float(fh) - nh, 0.0))
         out.append((nx, ny, nw, nh))
     return out
+
+
+def step_klt(state, luma_u8, t: int, dets, grid: int = 10, gate: float = 0.3,
+             min_score: float = 0.5):
+    """ftoracle.step with the KLT backend in place of flow + mean-box
+    predict: prediction runs on the processing-level frames (no
+    structure-texture); matching and the lifecycle are the reference's.
+    `state.prev_st` holds the previous processing-level frame."""
+    from dataclasses import replace
+    hh, ww = luma_u8.shape
+    lvl = O.select_level(ww, hh)
+    img = O.pyramid(O.gray8_to_unit(luma_u8), lvl + 1)[lvl]
+    if dets is not None:
+        dets = [d for d in dets if d.score >= min_score]
+    if state.prev_st is None:
+        if dets is not None:
+            state.tracks = O.update([], (), dets, t)
+    else:
+        act = [i for i, o in enumerate(state.tracks) if o.state == O.ACTIVE]
+        pred = klt_predict([state.tracks[i].box for i in act], state.prev_st, img, lvl,
+                           (ww, hh), grid)
+        for i, p in zip(act, pred):
+            if p is not None:
+                state.tracks[i] = replace(state.tracks[i], box=p)
+        if dets is not None:
+            cand = [i for i, p in zip(act, pred) if p is not None]
+            pairs, _, _ = O.match([state.tracks[i] for i in cand], dets, gate)
+            full = tuple((cand[i], j, s) for i, j, s in pairs)
+            state.tracks = O.update(state.tracks, full, dets, t)
+    state.prev_st = img
+    return state

@@ -47,7 +47,10 @@ class ft_tracker_config(C.Structure):
                 ("rof_iterations", C.c_int32), ("gate", C.c_double),
                 ("min_score", C.c_double), ("detection_blend", C.c_double),
                 ("rof_weight", C.c_double), ("rof_blend", C.c_double),
-                ("flow", ft_flow_params)]
+                ("flow", ft_flow_params), ("motion", C.c_int32), ("klt_grid", C.c_int32)]
+
+
+MOTION_TVL1, MOTION_KLT = 0, 1
 
 
 # numpy views of the record structs (same layout)

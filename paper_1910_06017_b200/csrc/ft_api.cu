@@ -604,6 +604,9 @@ struct ft_tracker {
   double *d_st = nullptr, *d_rofws = nullptr;
   double *d_pyr_prev = nullptr, *d_pyr_cur = nullptr, *d_fchain = nullptr;
   double *d_dx = nullptr, *d_dy = nullptr;
+  // KLT backend: pyramid geometry, per-point scratch, predicted boxes
+  Geometry kgeo;
+  double *d_kpts = nullptr, *d_kfwd = nullptr, *d_kfb = nullptr, *d_kbox = nullptr;
   ft_det *d_dets = nullptr;
   int32_t *d_in = nullptr;  // [0] = frame index, [1..S] = n_dets
   ft_track *d_out = nullptr;
@@ -692,6 +695,37 @@ struct ft_tracker {
       img = d_chain[L];
     }
     phase_mark("ingest+pyramid");
+    if (cfg.motion == FT_MOTION_KLT) {  // SURVEY 8 f4 backend: no ROF, no TV-L1
+      KltArgs ka;
+      FT_TRY(build_klt_pyramid(img, P, kgeo, d_pyr_cur, 3 * kgeo.total, S, s, ka.curr));
+      phase_mark("klt pyramid");
+      const double *kbox = nullptr;
+      if (has_prev) {
+        ka.prev = ka.curr;
+        ka.prev.lvl = d_pyr_prev;
+        ka.prev.gx = d_pyr_prev + kgeo.total;
+        ka.prev.gy = d_pyr_prev + 2 * kgeo.total;
+        ka.grid = cfg.klt_grid;
+        ka.max_pts = cfg.klt_grid * cfg.klt_grid;
+        ka.scale = (double)(1 << L);
+        FT_TRY(launch_klt_predict(ka, T.box, d_kbox, cfg.max_tracks, T.n_active, 0, S,
+                                  cfg.max_tracks, d_kpts, d_kfwd, d_kfb, T.valid, W, H, s));
+        kbox = d_kbox;
+        phase_mark("klt track");
+      }
+      FT_TRY(launch_tracker_track(T, nullptr, nullptr, P, PW, PH, L, dets, in + 1, in, has_prev,
+                                  d_out, d_nout, s, kbox));
+      phase_mark("predict+match+update");
+      FT_CUDA_TRY(cudaMemcpyAsync(d_pyr_prev, d_pyr_cur, (size_t)S * 3 * kgeo.total * 8,
+                                  cudaMemcpyDeviceToDevice, s));
+      if (host_io) {
+        FT_CUDA_TRY(cudaMemcpyAsync(h_out, d_out,
+                                    (size_t)S * 2 * cfg.max_tracks * sizeof(ft_track),
+                                    cudaMemcpyDeviceToHost, s));
+        FT_CUDA_TRY(cudaMemcpyAsync(h_nout, d_nout, (size_t)2 * S * 4, cudaMemcpyDeviceToHost, s));
+      }
+      return FT_OK;
+    }
     FT_TRY(launch_structure_texture(img, PW, PH, P, cfg.rof_weight, cfg.rof_blend,
                                     cfg.rof_iterations, d_st, P, d_rofws, 4 * P, S, s, 0, 0.25));
     phase_mark("structure_texture");
@@ -817,18 +851,34 @@ int ft_tracker_create(ft_ctx *ctx, const ft_tracker_config *cfg, ft_tracker **ou
     for (int l = 1; l <= t->L; ++l)
       FT_TRY(t->alloc(&t->d_chain[l], (size_t)S * t->lw[l] * t->lh[l]));
   }
-  FT_TRY(t->alloc(&t->d_st, (size_t)S * P));
-  FT_TRY(t->alloc(&t->d_rofws, (size_t)S * 4 * P));
-  FT_TRY(t->alloc(&t->d_pyr_prev, (size_t)S * t->geo.total));
-  FT_TRY(t->alloc(&t->d_pyr_cur, (size_t)S * t->geo.total));
-  FT_TRY(t->alloc(&t->d_fchain, (size_t)S * t->geo.total));
   FT_TRY(t->alloc(&t->d_dx, (size_t)S * P));
   FT_TRY(t->alloc(&t->d_dy, (size_t)S * P));
   FT_TRY(t->alloc(&t->d_dets, (size_t)S * cfg->max_dets));
   FT_TRY(t->alloc(&t->d_in, (size_t)S + 1));
   FT_TRY(t->alloc(&t->d_out, (size_t)S * 2 * cfg->max_tracks));
   FT_TRY(t->alloc(&t->d_nout, (size_t)2 * S));
-  FT_TRY(flow_work_alloc(t->fw, S, P));
+  if (cfg->motion == FT_MOTION_KLT) {
+    if (cfg->klt_grid < 1 || cfg->klt_grid > 11) return fail(FT_EINVAL, "klt_grid must be in 1..11");
+    FT_TRY(check_pyramid(t->PW, t->PH, kKltLevels));
+    t->kgeo.build(t->PW, t->PH, kKltLevels);
+    const size_t pyr = (size_t)S * 3 * t->kgeo.total;  // levels + gx + gy
+    FT_TRY(t->alloc(&t->d_pyr_prev, pyr));
+    FT_TRY(t->alloc(&t->d_pyr_cur, pyr));
+    const size_t pts = (size_t)S * cfg->max_tracks * cfg->klt_grid * cfg->klt_grid;
+    FT_TRY(t->alloc(&t->d_kpts, 2 * pts));
+    FT_TRY(t->alloc(&t->d_kfwd, 2 * pts));
+    FT_TRY(t->alloc(&t->d_kfb, pts));
+    FT_TRY(t->alloc(&t->d_kbox, (size_t)S * cfg->max_tracks * 4));
+  } else if (cfg->motion == FT_MOTION_TVL1) {
+    FT_TRY(t->alloc(&t->d_st, (size_t)S * P));
+    FT_TRY(t->alloc(&t->d_rofws, (size_t)S * 4 * P));
+    FT_TRY(t->alloc(&t->d_pyr_prev, (size_t)S * t->geo.total));
+    FT_TRY(t->alloc(&t->d_pyr_cur, (size_t)S * t->geo.total));
+    FT_TRY(t->alloc(&t->d_fchain, (size_t)S * t->geo.total));
+    FT_TRY(flow_work_alloc(t->fw, S, P));
+  } else {
+    return fail(FT_EINVAL, "motion must be FT_MOTION_TVL1 or FT_MOTION_KLT");
+  }
   // track tables
   TrackerDev &T = t->T;
   const int C = cfg->max_tracks, D = cfg->max_dets;
@@ -1054,6 +1104,7 @@ int ft_tracker_read_field(ft_tracker *t, int stream, double *h_dx, double *h_dy)
 int ft_tracker_profile_pd(ft_tracker *t, int reps, double *ms_per_launch, double *bytes_per_launch,
                           int *iters_per_launch) {
   if (!t || !ms_per_launch || reps < 1) return fail(FT_EINVAL, "bad argument");
+  if (t->cfg.motion != FT_MOTION_TVL1) return fail(FT_EINVAL, "no TV-L1 kernel in a KLT tracker");
   DeviceGuard g(t->ctx->device);
   FT_TRY(t->join_in());
   FT_CUDA_TRY(cudaStreamSynchronize(t->stream));

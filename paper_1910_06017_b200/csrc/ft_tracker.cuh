@@ -38,7 +38,8 @@ __device__ __forceinline__ void copy_track(TrackerDev &T, int64_t d, int64_t s) 
 int launch_tracker_track(TrackerDev &T, const double *dx, const double *dy, int64_t fstride,
                          int fw_l, int fh_l, int level, const ft_det *d_dets,
                          const int32_t *d_ndets, const int32_t *d_frame, bool has_prev,
-                         ft_track *d_out, int32_t *d_nout, cudaStream_t s);
+                         ft_track *d_out, int32_t *d_nout, cudaStream_t s,
+                         const double *kbox = nullptr);
 int tracker_kernel_setup(const TrackerDev &T);
 
 }  // namespace ft

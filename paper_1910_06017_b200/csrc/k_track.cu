@@ -516,15 +516,21 @@ __global__ void __launch_bounds__(32 * kPredWarps)
 
 // predict, phase 2: apply valid predictions (track.py:82-86), then build the
 // candidate list (actives with a prediction, table order) -- SURVEY A16 (4)
-__global__ void k_trk_apply(TrackerDev T, int level) {
+// kbox != null: the KLT backend already produced the predicted boxes
+__global__ void k_trk_apply(TrackerDev T, int level, const double *kbox) {
   const int s = blockIdx.x;
   const int na = T.n_active[s];
   const int64_t tb = (int64_t)s * T.cap;
   for (int i = threadIdx.x; i < na; i += blockDim.x) {
     const int64_t o = tb + i;
-    if (T.valid[o])
+    if (!T.valid[o]) continue;
+    if (kbox) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) T.box[4 * o + c] = kbox[4 * o + c];
+    } else {
       apply_shift(T.box + 4 * o, T.pmean[2 * o], T.pmean[2 * o + 1], level, T.frame_w, T.frame_h,
                   T.box + 4 * o);
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) {  // order-preserving compaction of candidates
@@ -708,13 +714,16 @@ __global__ void k_trk_pack(TrackerDev T, ft_track *out, int32_t *n_out) {
 int launch_tracker_track(TrackerDev &T, const double *dx, const double *dy, int64_t fstride,
                          int fw_l, int fh_l, int level, const ft_det *d_dets,
                          const int32_t *d_ndets, const int32_t *d_frame, bool has_prev,
-                         ft_track *d_out, int32_t *d_nout, cudaStream_t s) {
+                         ft_track *d_out, int32_t *d_nout, cudaStream_t s, const double *kbox) {
   const int S = T.n_streams;
-  if (has_prev) {
+  if (has_prev && kbox) {  // KLT backend: boxes + valid already predicted
+    k_trk_apply<<<S, 128, 0, s>>>(T, level, kbox);
+    count_launch();
+  } else if (has_prev) {
     const dim3 pg(S, (2 * T.cap + kPredWarps - 1) / kPredWarps);
     k_trk_predict<<<pg, 32 * kPredWarps, kPredWarps * sizeof(LeafScratch), s>>>(
         T, dx, dy, fstride, fw_l, fh_l, level);
-    k_trk_apply<<<S, 128, 0, s>>>(T, level);
+    k_trk_apply<<<S, 128, 0, s>>>(T, level, nullptr);
     count_launch(2);
   } else {
     // first frame: nothing to predict, every kept detection spawns

@@ -70,3 +70,25 @@ def test_klt_device_bit_exact():
     want1 = K.klt_predict(big, a, b, 1, (400, 300), grid=4)
     objs1 = [SceneObject(i, 0, "x", bx) for i, bx in enumerate(big)]
     assert predict_klt(objs1, Frame.from_array(a), Frame.from_array(b), 1, (400, 300), grid=4) == want1
+
+
+@pytest.mark.gpu
+def test_klt_tracker_matches_oracle():
+    """Tracker(motion="klt"): multi-stream lockstep step == oracle step_klt."""
+    from oracle import ftoracle as O
+    from paper_1910_06017_b200.pipeline import Tracker
+    from paper_1910_06017_b200.synth import make_sequence
+    from tests.goldutil import scene_rows
+    S, W, H, T = 2, 160, 120, 5
+    seqs = [make_sequence(W, H, 5, T, seed=70 + s, det_every=2, scale_change=True) for s in range(S)]
+    trk = Tracker(W, H, n_streams=S, motion="klt", klt_grid=5, max_tracks=64, max_dets=64)
+    states = [O.StreamState() for _ in range(S)]
+    for t in range(T):
+        frames = np.stack([seqs[s][0][t] for s in range(S)])
+        dets = [seqs[s][1][t] for s in range(S)]
+        scenes = trk.step(frames, t, dets)
+        for s in range(S):
+            od = None if dets[s] is None else [O.Det(d.class_id, d.label, d.score, d.box) for d in dets[s]]
+            K.step_klt(states[s], frames[s], t, od, grid=5)
+            assert np.array_equal(scene_rows(scenes[s]), scene_rows(states[s].tracks)), (s, t)
+    trk.close()

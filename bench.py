@@ -236,7 +236,7 @@ def run_ours(args, ws, rank, local):
 
     prm = FlowParams()
     trk = Tracker(W_, H_, n_streams=B, flow_params=prm, max_tracks=max_tracks, max_dets=max_dets,
-                  device=local)
+                  device=local, motion=args.motion, klt_grid=10)
     stream = torch.cuda.current_stream(dev)
 
     # ---------------- device-resident timing (value) ----------------
@@ -263,11 +263,13 @@ def run_ours(args, ws, rank, local):
 
     # ---------------- dominant kernel, timed alone ----------------
     msl, bpl, ipl = C_double(), C_double(), C_int()
-    _lib.check(trk._lib.ft_tracker_profile_pd(trk._h, 20, byref(msl), byref(bpl), byref(ipl)))
+    if args.motion == "tvl1":
+        _lib.check(trk._lib.ft_tracker_profile_pd(trk._h, 20, byref(msl), byref(bpl),
+                                                  byref(ipl)))
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     hbm = float(peaks.get("hbm_gbs", 6650.0))
-    achieved = bpl.value / (msl.value / 1000.0) / 1e9
+    achieved = bpl.value / (msl.value / 1000.0) / 1e9 if msl.value > 0 else 0.0
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "pd_traffic.json")
     if os.path.exists(tfile):
@@ -333,6 +335,13 @@ def run_ours(args, ws, rank, local):
                              "step_bytes_per_frame": frame_bytes},
                 "cpu_baseline": cpu, "clocks": clk.summary(),
                 "tracks_out": int(n_tracks)}
+        if args.motion == "klt":  # SURVEY 8 f4 backend: not the reference path
+            line["config"]["workload"] = (
+                "C2 with the KLT/MedianFlow backend (SURVEY 8 f4): 720x576 SD, 100 tracks, "
+                "10x10 points/box, 3-level LK pyramid, 9x9 window, forward-backward check, fp64")
+            line["config"]["l2"] = "per-stream KLT pyramids (~10 MB) re-read per step"
+            line["roofline"] = None  # gather-latency bound; no streaming-roofline model
+            line["step_roofline_frac"] = None
         print(json.dumps(line), flush=True)
 
 
@@ -346,6 +355,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--streams", type=int, default=32, help="SD streams per GPU")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--motion", choices=["tvl1", "klt"], default="tvl1",
+                    help="tvl1: the reference path (headline); klt: SURVEY 8 f4 backend")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget-s", type=float, default=150.0)
     args = ap.parse_args()

@@ -219,8 +219,15 @@ int ft_tracker_field(ft_tracker *trk, int stream, const double **d_dx, const dou
 int ft_tracker_read_field(ft_tracker *trk, int stream, double *h_dx, double *h_dy);
 /* Time the dominant kernel (finest-level primal-dual tile kernel) alone:
  * `reps` launches on the tracker's stream between CUDA events, over the state
- * the last step left.  bytes_per_launch = compulsory HBM bytes of a launch
- * (152 B per pixel per stream); iters_per_launch = PD iterations it fuses. */
+ * the last step left.  bytes_per_launch = SURVEY 8(d) algorithmic bytes of a
+ * launch (152 B per pixel-iteration x the pixel-iterations it performs);
+ * iters_per_launch = PD iterations it fuses. */
+/* Live timing of the dominant kernel inside the most recent step: CUDA
+ * events recorded (as graph nodes) around every finest-level primal-dual
+ * launch sequence of the step.  ms = summed device time of those launches,
+ * launches = their count, pixel_iters = pixel-iterations they performed over
+ * all streams (x 152 B = SURVEY 8(d) algorithmic bytes).  Synchronizes. */
+int ft_tracker_pd_span(ft_tracker *trk, double *ms, int *launches, double *pixel_iters);
 int ft_tracker_profile_pd(ft_tracker *trk, int reps, double *ms_per_launch,
                           double *bytes_per_launch, int *iters_per_launch);
 /* Kernel launches issued by the last step (for the bench's gpu_launches). */

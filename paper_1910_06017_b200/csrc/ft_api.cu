@@ -21,6 +21,7 @@ namespace ft {
 thread_local std::string g_err;
 thread_local LaunchCounter *g_launch_counter = nullptr;
 PhaseTimer *g_phase = nullptr;
+thread_local PdSpan *g_pd_span = nullptr;
 
 void PhaseTimer::report() {
   if (n < 2) return;
@@ -582,6 +583,7 @@ struct ft_tracker {
   // (ctx->stream) by events at entry and exit of every call
   cudaStream_t stream = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  PdSpan span;  // live finest-level PD timing (events baked into flow graphs)
   int join_in() {
     FT_CUDA_TRY(cudaEventRecord(ev_in, ctx->stream));
     FT_CUDA_TRY(cudaStreamWaitEvent(stream, ev_in, 0));
@@ -783,7 +785,9 @@ struct ft_tracker {
         g_launch_counter = nullptr;
         return cuda_fail(e, "cudaStreamBeginCapture");
       }
+      g_pd_span = span.ev[0] ? &span : nullptr;
       int rc = enqueue(s, has_prev, luma, dets, in, host_io);
+      g_pd_span = nullptr;
       e = cudaStreamEndCapture(s, &graph);
       g_launch_counter = nullptr;
       if (rc != FT_OK) {
@@ -825,6 +829,8 @@ int ft_tracker_create(ft_ctx *ctx, const ft_tracker_config *cfg, ft_tracker **ou
   FT_CUDA_TRY(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking));
   FT_CUDA_TRY(cudaEventCreateWithFlags(&t->ev_in, cudaEventDisableTiming));
   FT_CUDA_TRY(cudaEventCreateWithFlags(&t->ev_out, cudaEventDisableTiming));
+  if (cfg->motion == FT_MOTION_TVL1)
+    for (auto &e : t->span.ev) FT_CUDA_TRY(cudaEventCreate(&e));
   t->S = cfg->n_streams;
   t->W = cfg->width;
   t->H = cfg->height;
@@ -959,6 +965,8 @@ int ft_tracker_destroy(ft_tracker *t) {
     cudaFreeHost(sl.nout);
     if (sl.done) cudaEventDestroy(sl.done);
   }
+  for (auto &e : t->span.ev)
+    if (e) cudaEventDestroy(e);
   if (t->ev_in) cudaEventDestroy(t->ev_in);
   if (t->ev_out) cudaEventDestroy(t->ev_out);
   if (t->stream) cudaStreamDestroy(t->stream);
@@ -1119,6 +1127,23 @@ int ft_tracker_profile_pd(ft_tracker *t, int reps, double *ms_per_launch, double
   // across its iterations); bench.py reports that as compulsory bytes.
   if (bytes_per_launch) *bytes_per_launch = 152.0 * (double)t->P * t->S * iters;
   if (iters_per_launch) *iters_per_launch = iters;
+  return FT_OK;
+}
+
+int ft_tracker_pd_span(ft_tracker *t, double *ms, int *launches, double *pixel_iters) {
+  if (!t || !ms || !launches || !pixel_iters) return fail(FT_EINVAL, "NULL argument");
+  if (t->cfg.motion != FT_MOTION_TVL1) return fail(FT_EINVAL, "no TV-L1 kernel in a KLT tracker");
+  DeviceGuard g(t->ctx->device);
+  FT_CUDA_TRY(cudaStreamSynchronize(t->stream));
+  double tot = 0.0;
+  for (int wp = 0; wp < t->span.warps; ++wp) {
+    float m = 0.f;
+    FT_CUDA_TRY(cudaEventElapsedTime(&m, t->span.ev[2 * wp], t->span.ev[2 * wp + 1]));
+    tot += m;
+  }
+  *ms = tot;
+  *launches = t->span.launches;
+  *pixel_iters = (double)t->span.pixel_iters;
   return FT_OK;
 }
 

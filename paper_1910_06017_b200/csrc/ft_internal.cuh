@@ -118,6 +118,19 @@ struct PhaseTimer {
   void report();
 };
 extern PhaseTimer *g_phase;
+
+// Live timing of the dominant kernel inside the tracker step (bench.py's
+// roofline): run_flow records an event before the first and after the last
+// finest-level k_pd_tile launch of every warp.  Captured into the step
+// graph as event-record nodes, so the events hold the most recent replay.
+struct PdSpan {
+  static constexpr int kMaxWarps = 16;
+  cudaEvent_t ev[2 * kMaxWarps] = {};
+  int warps = 0;     // warps recorded in the captured step
+  int launches = 0;  // finest-level PD launches between the event pairs
+  int64_t pixel_iters = 0;  // pixel-iterations those launches perform (all images)
+};
+extern thread_local PdSpan *g_pd_span;
 inline void phase_mark(const char *what) {
   if (g_phase) g_phase->mark(what);
 }

@@ -228,6 +228,7 @@ struct PDArgs {
   int64_t cap;
   int halo, iters, first, nb;
   int pow2;  // sigma and tau are powers of two (exact fused multiply-adds)
+  int cone;  // compute only the rows feeding the written interior (FT_PD_CONE)
   double tau, lam, sigma, shrink;  // shrink = 1/(1+sigma*eps)
 };
 
@@ -275,17 +276,33 @@ __device__ __forceinline__ void pd_iterate(int iters, double *sm, int base, int 
                                            const double *gx, const double *gy, const double *r0,
                                            const double *thr, const double *ig2, double tau,
                                            double tl, double sigma, double shrink, double2 *queue,
-                                           X &xch) {
+                                           X &xch, int ty = 0, int cone = -1) {
   using G = PDGeom<TW, BY, PY>;
-  constexpr int NX = G::NX, NP = G::NP, SP = G::SP, PL = G::PLANE;
+  constexpr int NX = G::NX, NP = G::NP, SP = G::SP, PL = G::PLANE, TH = G::TH;
   double2 *const sB = reinterpret_cast<double2 *>(sm), *const sPX = sB + PL, *const sPY = sPX + PL;
   const unsigned lt_mask = (1u << tx) - 1u;
   for (int it = 0; it < iters; ++it) {
     double p11[NP], p12[NP], p21[NP], p22[NP];
+    // Shrinking cone (cone = halo - iters >= 0, tiles with a halo): only the
+    // rows that feed the written interior [halo, TH-halo) are computed.
+    // Iteration it needs p on rows [cone+it, TH-1-cone-it) and u on
+    // [cone+it+1, TH-1-cone-it); a row is one warp, so the skip is
+    // warp-uniform.  Values outside the cone are never read by rows inside.
+    bool dual_row[NP], primal_row[NP];
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      const int lr = ty + BY * (q / NX);
+      dual_row[q] = cone < 0 || (lr >= cone + it && lr < TH - 1 - cone - it);
+      primal_row[q] = cone < 0 || (lr >= cone + it + 1 && lr < TH - 1 - cone - it);
+    }
     // ---- dual ascent with Huber prox (:180-185); the apron makes the
     // neighbour loads safe, the border flags select the reference's zeros
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
+      if (!dual_row[q]) {
+        p11[q] = p12[q] = p21[q] = p22[q] = 0.0;  // not projected, not stored
+        continue;
+      }
       const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
       const double2 cb = sB[id], rb = sB[id + 1], db = sB[id + SP];
       const double2 opx = sPX[id], opy = sPY[id];
@@ -353,6 +370,7 @@ __device__ __forceinline__ void pd_iterate(int iters, double *sm, int base, int 
     }
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
+      if (!dual_row[q]) continue;
       const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
       sPX[id] = make_double2(p11[q], p21[q]);  // in place: only the owner reads p here
       sPY[id] = make_double2(p12[q], p22[q]);
@@ -361,6 +379,7 @@ __device__ __forceinline__ void pd_iterate(int iters, double *sm, int base, int 
     // ---- primal descent + TV-L1 shrinkage (:194-208)
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
+      if (!primal_row[q]) continue;
       const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
       const unsigned f = fl[q];
       // divergence (imageops.py:41-50): dx + dy with border rules
@@ -481,9 +500,10 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const PDArgs a) {
   BlockBarrier bar;
   // tile free of image-border pixels (uniform per CTA): flag-free fast path
   const bool interior = ox >= 1 && oy >= 1 && ox + TW <= W - 1 && oy + TH <= H - 1;
+  const int cone = a.cone && a.halo > 0 && a.iters <= a.halo ? a.halo - a.iters : -1;
 #define FT_PD_CALL(P2_, IN_)                                                                  \
   pd_iterate<TW, BY, PY, P2_, IN_>(a.iters, sm, base, tx, fl, u1, u2, gx, gy, r0, thr, ig2,   \
-                                   a.tau, tl, a.sigma, a.shrink, queue, bar)
+                                   a.tau, tl, a.sigma, a.shrink, queue, bar, ty, cone)
   if (a.pow2) {
     if (interior) FT_PD_CALL(true, true); else FT_PD_CALL(true, false);
   } else {
@@ -1219,6 +1239,7 @@ int profile_pd(FlowWork &fw, int w, int h, int nb, const FlowParamsD &p, int rep
   a.first = 0;
   a.nb = nb;
   a.pow2 = pow2_params(p.tau);
+  a.cone = env_int("FT_PD_CONE", 1);
   a.tau = p.tau;
   a.lam = p.lam;
   a.sigma = 1.0 / (8.0 * p.tau);
@@ -1352,6 +1373,11 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
       k_warp_setup<<<grid2d(w, h, nb), blk, 0, s>>>(i0, i1, pyr_stride, fw.ix, fw.iy, st.p[U1],
                                                      st.p[U2], w, h, cap, fw.gx, fw.gy, fw.r0);
       count_launch();
+      PdSpan *span = lvl == 0 && !resident && wp < PdSpan::kMaxWarps ? g_pd_span : nullptr;
+      if (span) {
+        if (wp == 0) span->warps = span->launches = 0, span->pixel_iters = 0;
+        FT_CUDA_TRY(cudaEventRecord(span->ev[2 * wp], s));
+      }
       int done = 0;
       while (done < p.iters) {
         const int n = resident ? p.iters : std::min(halo, p.iters - done);
@@ -1369,6 +1395,7 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
         a.first = done == 0;
         a.nb = nb;
         a.pow2 = pow2_params(p.tau);
+        a.cone = env_int("FT_PD_CONE", 1);
         a.tau = p.tau;
         a.lam = p.lam;
         a.sigma = sigma;
@@ -1376,6 +1403,12 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
         FT_TRY(pd_launch(plan.cfg, a, nb, s));
         cur = 1 - cur;
         done += n;
+        if (span) ++span->launches;
+      }
+      if (span) {
+        FT_CUDA_TRY(cudaEventRecord(span->ev[2 * wp + 1], s));
+        span->warps = wp + 1;
+        span->pixel_iters += (int64_t)w * h * nb * p.iters;
       }
       StatePtrs in = state_ptrs(fw.st[cur], fw.nb, cap);
       StatePtrs out = state_ptrs(fw.st[1 - cur], fw.nb, cap);

@@ -7,6 +7,8 @@
 #include "ft_internal.cuh"
 #include "ft_klt.cuh"
 
+#include <cstdlib>
+
 namespace ft {
 
 namespace {
@@ -103,7 +105,8 @@ constexpr int kPtWarps = 8;
 // one warp per (stream, box, point): forward LK, then backward LK from the
 // forward result; writes the grid point, its forward position and the
 // forward-backward error (-1 when lost either way)
-__global__ void __launch_bounds__(32 * kPtWarps)
+template <int MINB>
+__global__ void __launch_bounds__(32 * kPtWarps, MINB)
     k_klt_points(KltArgs a, const double *boxes, int64_t box_stride, const int32_t *n_boxes,
                  int n_boxes_const, double *pts, double *fwd, double *fb) {
   const int s = blockIdx.y;
@@ -272,8 +275,18 @@ int launch_klt_predict(const KltArgs &a, const double *boxes, double *out_boxes,
   if (a.grid < 1 || a.grid * a.grid > 128) return fail(FT_EINVAL, "klt grid must be 1..11");
   const int items = max_boxes * a.grid * a.grid;
   if (items == 0) return FT_OK;
-  k_klt_points<<<dim3((items + kPtWarps - 1) / kPtWarps, n_streams), 32 * kPtWarps, 0, s>>>(
-      a, boxes, box_stride, n_boxes, n_boxes_const, pts, fwd, fb);
+  // resident CTAs per SM requested from ptxas (register cap); FT_KLT_MINB
+  static const int minb = [] {
+    const char *e = getenv("FT_KLT_MINB");
+    return e ? atoi(e) : 2;
+  }();
+  const dim3 grid((items + kPtWarps - 1) / kPtWarps, n_streams);
+  if (minb >= 4)
+    k_klt_points<4><<<grid, 32 * kPtWarps, 0, s>>>(a, boxes, box_stride, n_boxes, n_boxes_const, pts, fwd, fb);
+  else if (minb == 3)
+    k_klt_points<3><<<grid, 32 * kPtWarps, 0, s>>>(a, boxes, box_stride, n_boxes, n_boxes_const, pts, fwd, fb);
+  else
+    k_klt_points<2><<<grid, 32 * kPtWarps, 0, s>>>(a, boxes, box_stride, n_boxes, n_boxes_const, pts, fwd, fb);
   k_klt_boxes<<<dim3((max_boxes + kPtWarps - 1) / kPtWarps, n_streams), 32 * kPtWarps, 0, s>>>(
       a, boxes, out_boxes, box_stride, n_boxes, n_boxes_const, pts, fwd, fb, valid, frame_w,
       frame_h);

@@ -52,6 +52,25 @@ def launches(path):
     return "\n".join(out)
 
 
+def pick(path, kernel="k_pd_tile"):
+    """ncu -s value selecting the 2nd launch of `kernel` with the largest grid
+    (the finest level, not the first launch of a warp) in a launch list."""
+    rows = list(csv.reader(open(path)))
+    hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+    h = rows[hi]
+    ki, gi = h.index("Kernel Name"), h.index("Grid Size")
+    seq = [r[gi] for r in rows[hi + 1:] if len(r) > gi and kernel in r[ki]]
+
+    def cells(g):
+        n = 1
+        for x in g.strip("()").split(","):
+            n *= int(x)
+        return n
+    big = max(cells(g) for g in seq)
+    hits = [i for i, g in enumerate(seq) if cells(g) == big]
+    return hits[1]
+
+
 def ncu_csv(report, *args):
     res = subprocess.run(["ncu", "-i", report, *args, "--csv"], capture_output=True, text=True)
     return list(csv.reader(io.StringIO(res.stdout)))
@@ -105,10 +124,14 @@ def main():
     ap.add_argument("--launches")
     ap.add_argument("--report")
     ap.add_argument("--tag", default="r01")
+    ap.add_argument("--pick", help="launch list: print the ncu -s index of a finest PD launch")
     ap.add_argument("--note", default="")
     ap.add_argument("--stream-pixels", type=float, default=0.0,
                     help="streams x pixels of the captured launch (normalises traffic)")
     a = ap.parse_args()
+    if a.pick:
+        print(pick(a.pick))
+        return
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     if a.launches:
         md = launches(a.launches)

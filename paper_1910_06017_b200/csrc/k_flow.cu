@@ -1376,7 +1376,7 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
       PdSpan *span = lvl == 0 && !resident && wp < PdSpan::kMaxWarps ? g_pd_span : nullptr;
       if (span) {
         if (wp == 0) span->warps = span->launches = 0, span->pixel_iters = 0;
-        FT_CUDA_TRY(cudaEventRecord(span->ev[2 * wp], s));
+        FT_CUDA_TRY(cudaEventRecordWithFlags(span->ev[2 * wp], s, cudaEventRecordExternal));
       }
       int done = 0;
       while (done < p.iters) {
@@ -1406,7 +1406,7 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
         if (span) ++span->launches;
       }
       if (span) {
-        FT_CUDA_TRY(cudaEventRecord(span->ev[2 * wp + 1], s));
+        FT_CUDA_TRY(cudaEventRecordWithFlags(span->ev[2 * wp + 1], s, cudaEventRecordExternal));
         span->warps = wp + 1;
         span->pixel_iters += (int64_t)w * h * nb * p.iters;
       }

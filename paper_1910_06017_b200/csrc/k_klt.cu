@@ -278,7 +278,7 @@ int launch_klt_predict(const KltArgs &a, const double *boxes, double *out_boxes,
   // resident CTAs per SM requested from ptxas (register cap); FT_KLT_MINB
   static const int minb = [] {
     const char *e = getenv("FT_KLT_MINB");
-    return e ? atoi(e) : 2;
+    return e ? atoi(e) : 3;
   }();
   const dim3 grid((items + kPtWarps - 1) / kPtWarps, n_streams);
   if (minb >= 4)

@@ -229,6 +229,7 @@ struct PDArgs {
   int halo, iters, first, nb;
   int pow2;  // sigma and tau are powers of two (exact fused multiply-adds)
   int cone;  // compute only the rows feeding the written interior (FT_PD_CONE)
+  int cq;    // CTA-wide projection queue (FT_PD_CQ)
   double tau, lam, sigma, shrink;  // shrink = 1/(1+sigma*eps)
 };
 
@@ -409,6 +410,125 @@ __device__ __forceinline__ void pd_iterate(int iters, double *sm, int base, int 
   }
 }
 
+// Same iteration with a CTA-wide projection queue (k_pd_tile): the dual step
+// stores its unprojected p, the saturated pairs of the whole CTA (~9 % of
+// pairs at C2) are appended to one shared index list, and after a barrier
+// the first ceil(n/32) warps project them in place -- instead of every warp
+// running the hypot + division code for its own ~4 saturated pairs with most
+// lanes idle.  The primal step re-reads its own p from shared memory, so p
+// is not held in registers across the barriers.  Bit-identical to
+// pd_iterate: the same pairs get the same max(1, hypot) and divisions.
+template <int TW, int BY, int PY, bool P2, bool IN>
+__device__ __forceinline__ void pd_iterate_cq(int iters, double *sm, int base, int tx, int ty,
+                                              const unsigned *fl, double *u1, double *u2,
+                                              const double *gx, const double *gy,
+                                              const double *r0, const double *thr,
+                                              const double *ig2, double tau, double tl,
+                                              double sigma, double shrink, int *qidx, int *ctr,
+                                              int cone) {
+  using G = PDGeom<TW, BY, PY>;
+  constexpr int NX = G::NX, NP = G::NP, SP = G::SP, PL = G::PLANE, TH = G::TH;
+  constexpr int NT = 32 * BY;
+  double2 *const sB = reinterpret_cast<double2 *>(sm), *const sPX = sB + PL, *const sPY = sPX + PL;
+  double *const dPX = reinterpret_cast<double *>(sPX), *const dPY = reinterpret_cast<double *>(sPY);
+  const unsigned lt_mask = (1u << tx) - 1u;
+  const int tid = ty * 32 + tx;
+  for (int it = 0; it < iters; ++it) {
+    bool dual_row[NP], primal_row[NP];
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {  // shrinking cone, as in pd_iterate
+      const int lr = ty + BY * (q / NX);
+      dual_row[q] = cone < 0 || (lr >= cone + it && lr < TH - 1 - cone - it);
+      primal_row[q] = cone < 0 || (lr >= cone + it + 1 && lr < TH - 1 - cone - it);
+    }
+    // ---- dual ascent with Huber prox (:180-185), unprojected p stored in place
+    unsigned need = 0;
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      if (!dual_row[q]) continue;
+      const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
+      const double2 cb = sB[id], rb = sB[id + 1], db = sB[id + SP];
+      const double2 opx = sPX[id], opy = sPY[id];
+      const bool R = IN || (fl[q] & FL_R), D = IN || (fl[q] & FL_D);
+      const double a1x = R ? rb.x - cb.x : 0.0;
+      const double a1y = D ? db.x - cb.x : 0.0;
+      const double a2x = R ? rb.y - cb.y : 0.0;
+      const double a2y = D ? db.y - cb.y : 0.0;
+      const double p11 = madx<P2>(sigma, a1x, opx.x) * shrink;
+      const double p12 = madx<P2>(sigma, a1y, opy.x) * shrink;
+      const double p21 = madx<P2>(sigma, a2x, opx.y) * shrink;
+      const double p22 = madx<P2>(sigma, a2y, opy.y) * shrink;
+      sPX[id] = make_double2(p11, p21);
+      sPY[id] = make_double2(p12, p22);
+      // screening test only (not reference arithmetic): fused is fine
+      if (fma(p11, p11, p12 * p12) > 0.999999) need |= 1u << (2 * q);
+      if (fma(p21, p21, p22 * p22) > 0.999999) need |= 1u << (2 * q + 1);
+    }
+    // ---- append saturated pairs: one shared atomic per warp
+    int off[2 * NP];
+    int total = 0;
+    if (__any_sync(0xffffffffu, need != 0u)) {
+#pragma unroll
+      for (int j = 0; j < 2 * NP; ++j) {
+        const unsigned m = __ballot_sync(0xffffffffu, (need >> j) & 1u);
+        off[j] = total + __popc(m & lt_mask);
+        total += __popc(m);
+      }
+      int wbase = 0;
+      if (tx == 0) wbase = atomicAdd(&ctr[it & 1], total);
+      wbase = __shfl_sync(0xffffffffu, wbase, 0);
+#pragma unroll
+      for (int j = 0; j < 2 * NP; ++j) {
+        const int q = j >> 1;
+        const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
+        if ((need >> j) & 1u) qidx[wbase + off[j]] = 2 * id + (j & 1);
+      }
+    }
+    __syncthreads();
+    // ---- unit-ball projection n = max(1, hypot(.)); p /= n (:186-191)
+    const int n = ctr[it & 1];
+    if (tid == 0) ctr[(it + 1) & 1] = 0;  // next iteration's list (unused until then)
+    for (int e = tid; e < n; e += NT) {
+      const int k = qidx[e];
+      const double a = dPX[k], b = dPY[k];
+      const double nn = np_max(1.0, glibc_hypot(a, b));
+      dPX[k] = a / nn;
+      dPY[k] = b / nn;
+    }
+    __syncthreads();
+    // ---- primal descent + TV-L1 shrinkage (:194-208)
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      if (!primal_row[q]) continue;
+      const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
+      const unsigned f = fl[q];
+      const double2 mpx = sPX[id], mpy = sPY[id];
+      const double p11 = mpx.x, p21 = mpx.y, p12 = mpy.x, p22 = mpy.y;
+      const double2 lp = sPX[id - 1], up = sPY[id - SP];
+      const double l11 = lp.x, l21 = lp.y, u12 = up.x, u22 = up.y;
+      const bool L = IN || (f & FL_L), LC = !IN && (f & FL_LASTC);
+      const bool U = IN || (f & FL_U), LR = !IN && (f & FL_LASTR);
+      const double dx1 = L ? (LC ? -l11 : p11 - l11) : p11;
+      const double dx2 = L ? (LC ? -l21 : p21 - l21) : p21;
+      const double dy1 = U ? (LR ? -u12 : p12 - u12) : p12;
+      const double dy2 = U ? (LR ? -u22 : p22 - u22) : p22;
+      const double v1 = madx<P2>(tau, dx1 + dy1, u1[q]);
+      const double v2 = madx<P2>(tau, dx2 + dy2, u2[q]);
+      const double rho = r0[q] + gx[q] * v1 + gy[q] * v2;
+      const bool lo = rho < -thr[q];
+      const bool hi = rho > thr[q];
+      double d = lo ? tl : (hi ? -tl : -rho * ig2[q]);
+      d = (ig2[q] != 0.0 || lo || hi) ? d : 0.0;  // ig2 != 0 <=> |grad|^2 > 1e-12
+      const double n1 = v1 + d * gx[q];
+      const double n2 = v2 + d * gy[q];
+      sB[id] = make_double2(madx<true>(2.0, n1, -u1[q]), madx<true>(2.0, n2, -u2[q]));
+      u1[q] = n1;
+      u2[q] = n2;
+    }
+    __syncthreads();
+  }
+}
+
 struct BlockBarrier {
   __device__ __forceinline__ void after_dual() { __syncthreads(); }
   __device__ __forceinline__ void after_primal() { __syncthreads(); }
@@ -494,6 +614,7 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const PDArgs a) {
       sm[sxi(5, id, PL)] = q22;
     }
   }
+  if (tid < 2) reinterpret_cast<int *>(sm + 6 * PL)[2 * NP * 32 * BY + tid] = 0;  // queue counters
   __syncthreads();
 
   double2 *const queue = reinterpret_cast<double2 *>(sm + 6 * PL) + ty * (2 * NP * 32);
@@ -501,15 +622,29 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const PDArgs a) {
   // tile free of image-border pixels (uniform per CTA): flag-free fast path
   const bool interior = ox >= 1 && oy >= 1 && ox + TW <= W - 1 && oy + TH <= H - 1;
   const int cone = a.cone && a.halo > 0 && a.iters <= a.halo ? a.halo - a.iters : -1;
+  if (a.cq) {
+    int *const qidx = reinterpret_cast<int *>(sm + 6 * PL);
+    int *const ctr = qidx + 2 * NP * 32 * BY;
+#define FT_PD_CALL(P2_, IN_)                                                                  \
+  pd_iterate_cq<TW, BY, PY, P2_, IN_>(a.iters, sm, base, tx, ty, fl, u1, u2, gx, gy, r0, thr, \
+                                      ig2, a.tau, tl, a.sigma, a.shrink, qidx, ctr, cone)
+    if (a.pow2) {
+      if (interior) FT_PD_CALL(true, true); else FT_PD_CALL(true, false);
+    } else {
+      if (interior) FT_PD_CALL(false, true); else FT_PD_CALL(false, false);
+    }
+#undef FT_PD_CALL
+  } else {
 #define FT_PD_CALL(P2_, IN_)                                                                  \
   pd_iterate<TW, BY, PY, P2_, IN_>(a.iters, sm, base, tx, fl, u1, u2, gx, gy, r0, thr, ig2,   \
                                    a.tau, tl, a.sigma, a.shrink, queue, bar, ty, cone)
-  if (a.pow2) {
-    if (interior) FT_PD_CALL(true, true); else FT_PD_CALL(true, false);
-  } else {
-    if (interior) FT_PD_CALL(false, true); else FT_PD_CALL(false, false);
-  }
+    if (a.pow2) {
+      if (interior) FT_PD_CALL(true, true); else FT_PD_CALL(true, false);
+    } else {
+      if (interior) FT_PD_CALL(false, true); else FT_PD_CALL(false, false);
+    }
 #undef FT_PD_CALL
+  }
 
   // ---- write back the exact interior
   const int lo_x = a.halo, hi_x = TW - a.halo;
@@ -1240,6 +1375,7 @@ int profile_pd(FlowWork &fw, int w, int h, int nb, const FlowParamsD &p, int rep
   a.nb = nb;
   a.pow2 = pow2_params(p.tau);
   a.cone = env_int("FT_PD_CONE", 1);
+  a.cq = env_int("FT_PD_CQ", 1);
   a.tau = p.tau;
   a.lam = p.lam;
   a.sigma = 1.0 / (8.0 * p.tau);
@@ -1396,6 +1532,7 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
         a.nb = nb;
         a.pow2 = pow2_params(p.tau);
         a.cone = env_int("FT_PD_CONE", 1);
+        a.cq = env_int("FT_PD_CQ", 1);
         a.tau = p.tau;
         a.lam = p.lam;
         a.sigma = sigma;

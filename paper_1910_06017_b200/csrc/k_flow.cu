@@ -1187,6 +1187,7 @@ struct PDConfig {
   void (*fn)(PDArgs);
   size_t smem;
   bool persistent = false;
+  size_t smem_cq = 0;  // k_pd_tile with the CTA-wide queue (PDArgs::cq)
 };
 
 template <int TW, int BY, int PY>
@@ -1204,7 +1205,9 @@ PDConfig make_strip_cfg(int idx) {
 template <int TW, int BY, int PY, int MINB>
 PDConfig make_cfg(int idx) {
   using G = PDGeom<TW, BY, PY>;
-  return PDConfig{idx, TW, G::TH, BY, &k_pd_tile<TW, BY, PY, MINB>, G::smem};
+  PDConfig c{idx, TW, G::TH, BY, &k_pd_tile<TW, BY, PY, MINB>, G::smem};
+  c.smem_cq = 6 * G::PLANE * sizeof(double) + (2 * G::NP * 32 * BY + 2) * sizeof(int);
+  return c;
 }
 
 // index: 0 = 32x32/256thr, 1 = 32x32/512thr, 2 = 64x32/512thr, 3 = 64x32/256thr
@@ -1251,7 +1254,10 @@ int pd_launch(const PDConfig &c, const PDArgs &a, int nb, cudaStream_t s) {
     count_launch();
     return FT_OK;
   }
-  c.fn<<<grid, dim3(32, c.by), c.smem, s>>>(a);
+  // the CTA-wide projection queue needs 4 B per pair instead of the per-warp
+  // 16 B: smaller carve-out, larger L1
+  const size_t smem = a.cq && c.smem_cq ? c.smem_cq : c.smem;
+  c.fn<<<grid, dim3(32, c.by), smem, s>>>(a);
   count_launch();
   return FT_OK;
 }

@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(32 * kRBY, 2)
     k_rof_tile(const double *__restrict__ img, int w, int h, int64_t is,
                const double *__restrict__ px_in, const double *__restrict__ py_in,
                double *__restrict__ px_out, double *__restrict__ py_out, int64_t ps,
-               double weight, double step, int halo, int iters, int first) {
+               double weight, double step, int halo, int iters, int first, int cone_on) {
   __shared__ double s_px[kRPL], s_py[kRPL], s_d[kRPL];
   const int step_x = kRTW - 2 * halo, step_y = kRTH - 2 * halo;
   const int ox = blockIdx.x * step_x - halo, oy = blockIdx.y * step_y - halo;
@@ -200,10 +200,16 @@ __global__ void __launch_bounds__(32 * kRBY, 2)
     s_py[id] = py[k];
   }
   __syncthreads();
+  // Shrinking cone (tiles with a halo): iteration it (0-based) needs p on
+  // rows [c+it+1, TH-c-it-1) and d on [c+it+1, TH-c-it), c = halo - iters,
+  // for the written interior [halo, TH-halo); a row is one warp.
+  const int cone = (cone_on && halo > 0 && iters <= halo) ? halo - iters : -1;
   for (int it = 0; it < iters; ++it) {
     double d[kRPY];
 #pragma unroll
     for (int k = 0; k < kRPY; ++k) {  // d = divergence(p) - img/weight
+      const int lr = ty + kRBY * k;
+      if (cone >= 0 && (lr < cone + it + 1 || lr >= kRTH - cone - it)) continue;
       const int id = (ty + kRBY * k + 1) * kRSP + tx + 1;
       const double l = s_px[id - 1], u = s_py[id - kRSP];
       const double dx = fL[k] ? (fLC[k] ? -l : px[k] - l) : px[k];
@@ -214,6 +220,8 @@ __global__ void __launch_bounds__(32 * kRBY, 2)
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < kRPY; ++k) {  // g = forward_gradient(d); p update
+      const int lr = ty + kRBY * k;
+      if (cone >= 0 && (lr < cone + it + 1 || lr >= kRTH - cone - it - 1)) continue;
       const int id = (ty + kRBY * k + 1) * kRSP + tx + 1;
       const double gx = fR[k] ? s_d[id + 1] - d[k] : 0.0;
       const double gy = fD[k] ? s_d[id + kRSP] - d[k] : 0.0;
@@ -304,6 +312,8 @@ int launch_structure_texture(const double *img, int w, int h, int64_t is, double
     const int halo_t = (hv && *hv) ? atoi(hv) : 4;
     const bool resident = w <= kRTW && h <= kRTH;
     const int halo = resident ? 0 : halo_t;
+    const char *cv = getenv("FT_ROF_CONE");
+    const int cone_on = (cv && *cv) ? atoi(cv) : 1;
     const int sx = kRTW - 2 * halo, sy = kRTH - 2 * halo;
     const dim3 g(resident ? 1 : (w + sx - 1) / sx, resident ? 1 : (h + sy - 1) / sy, nb);
     int done = 0;
@@ -313,7 +323,8 @@ int launch_structure_texture(const double *img, int w, int h, int64_t is, double
       const bool p2 = step > 0.0 && std::frexp(step, &e2) == 0.5;
       auto kern = p2 ? k_rof_tile<true> : k_rof_tile<false>;
       kern<<<g, dim3(32, kRBY), 0, s>>>(img, w, h, is, p[cur][0], p[cur][1], p[1 - cur][0],
-                                        p[1 - cur][1], wss, weight, step, halo, k, done == 0);
+                                        p[1 - cur][1], wss, weight, step, halo, k, done == 0,
+                                        cone_on);
       count_launch();
       cur = 1 - cur;
       done += k;

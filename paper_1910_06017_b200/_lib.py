@@ -13,7 +13,7 @@ import threading
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libomnitrack.so")
+LIB_PATH = os.environ.get("FT_LIB") or os.path.join(HERE, "libomnitrack.so")  # FT_LIB: A/B builds
 
 FT_OK, FT_EINVAL, FT_ERANGE, FT_ECUDA, FT_ENOMEM, FT_ECAP = 0, -1, -2, -3, -4, -5
 

@@ -230,6 +230,7 @@ struct PDArgs {
   int pow2;  // sigma and tau are powers of two (exact fused multiply-adds)
   int cone;  // compute only the rows feeding the written interior (FT_PD_CONE)
   int cq;    // CTA-wide projection queue (FT_PD_CQ)
+  int async_ld;  // exchange planes loaded with cp.async (FT_PD_ASYNC)
   double tau, lam, sigma, shrink;  // shrink = 1/(1+sigma*eps)
 };
 
@@ -529,6 +530,17 @@ __device__ __forceinline__ void pd_iterate_cq(int iters, double *sm, int base, i
   }
 }
 
+// global -> shared copies without register staging (LDGSTS)
+__device__ __forceinline__ void cp_async8(double *dst, const double *src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const int n = valid ? 8 : 0;  // src-size 0: zero-fill the 8 bytes
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
 struct BlockBarrier {
   __device__ __forceinline__ void after_dual() { __syncthreads(); }
   __device__ __forceinline__ void after_primal() { __syncthreads(); }
@@ -573,6 +585,15 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const PDArgs a) {
       const int gc = ox + tx + 32 * cx, gr = oy + ty + BY * k;
       const bool in = gc >= 0 && gc < W && gr >= 0 && gr < H;
       const int64_t o = so + (int64_t)gr * W + gc;
+      const int id = base + k * BY * SP + 32 * cx;
+      // exchange planes go straight to shared memory (cp.async, zero-filled
+      // outside the image): no registers held, all copies in flight at once
+      const bool async_x = a.async_ld && !a.first;
+      if (async_x) {
+#pragma unroll
+        for (int f = 0; f < 6; ++f)
+          cp_async8(&sm[sxi(f, id, PL)], in ? a.in.p[B1 + f] + o : a.in.p[B1 + f], in);
+      }
       double vu1 = 0, vu2 = 0, vb1 = 0, vb2 = 0, q11 = 0, q12 = 0, q21 = 0, q22 = 0;
       double vgx = 0, vgy = 0, vr0 = 0;
       if (in) {
@@ -581,7 +602,7 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const PDArgs a) {
         if (a.first) {
           vb1 = vu1;  // ub = u, p = 0 at the start of a warp (optflow.py:169-174)
           vb2 = vu2;
-        } else {
+        } else if (!async_x) {
           vb1 = a.in.p[B1][o];
           vb2 = a.in.p[B2][o];
           q11 = a.in.p[P11][o];
@@ -605,15 +626,17 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const PDArgs a) {
       fl[q] = (gc < W - 1 ? FL_R : 0u) | (gr < H - 1 ? FL_D : 0u) | (gc > 0 ? FL_L : 0u) |
               (gc == W - 1 ? FL_LASTC : 0u) | (gr > 0 ? FL_U : 0u) | (gr == H - 1 ? FL_LASTR : 0u) |
               (ok ? FL_OK : 0u);
-      const int id = base + k * BY * SP + 32 * cx;
-      sm[sxi(0, id, PL)] = vb1;
-      sm[sxi(1, id, PL)] = vb2;
-      sm[sxi(2, id, PL)] = q11;
-      sm[sxi(3, id, PL)] = q12;
-      sm[sxi(4, id, PL)] = q21;
-      sm[sxi(5, id, PL)] = q22;
+      if (!async_x) {
+        sm[sxi(0, id, PL)] = vb1;
+        sm[sxi(1, id, PL)] = vb2;
+        sm[sxi(2, id, PL)] = q11;
+        sm[sxi(3, id, PL)] = q12;
+        sm[sxi(4, id, PL)] = q21;
+        sm[sxi(5, id, PL)] = q22;
+      }
     }
   }
+  if (a.async_ld && !a.first) cp_async_wait_all();
   if (tid < 2) reinterpret_cast<int *>(sm + 6 * PL)[2 * NP * 32 * BY + tid] = 0;  // queue counters
   __syncthreads();
 
@@ -1053,15 +1076,6 @@ struct PersistGeom {
                                  BY * 2 * G::NP * 32 * 16;
 };
 
-__device__ __forceinline__ void cp_async8(double *dst, const double *src, bool valid) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  const int n = valid ? 8 : 0;  // src-size 0: zero-fill the 8 bytes
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(n));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-}
 
 template <int TW, int BY, int PY>
 __global__ void __launch_bounds__(32 * BY, 1) k_pd_persist(const PDArgs a) {
@@ -1382,6 +1396,7 @@ int profile_pd(FlowWork &fw, int w, int h, int nb, const FlowParamsD &p, int rep
   a.pow2 = pow2_params(p.tau);
   a.cone = env_int("FT_PD_CONE", 1);
   a.cq = env_int("FT_PD_CQ", 1);
+  a.async_ld = env_int("FT_PD_ASYNC", 1);
   a.tau = p.tau;
   a.lam = p.lam;
   a.sigma = 1.0 / (8.0 * p.tau);
@@ -1539,6 +1554,7 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
         a.pow2 = pow2_params(p.tau);
         a.cone = env_int("FT_PD_CONE", 1);
         a.cq = env_int("FT_PD_CQ", 1);
+        a.async_ld = env_int("FT_PD_ASYNC", 1);
         a.tau = p.tau;
         a.lam = p.lam;
         a.sigma = sigma;

@@ -444,9 +444,9 @@ __device__ __forceinline__ void pd_iterate_cq(int iters, double *sm, int base, i
     }
     // ---- dual ascent with Huber prox (:180-185), unprojected p stored in place
     unsigned need = 0;
-#pragma unroll
-    for (int q = 0; q < NP; ++q) {
-      if (!dual_row[q]) continue;
+    // (the common all-rows-active case runs branch-free so the compiler can
+    // interleave the pixels' dependency chains)
+    auto dual_px = [&](const int q) {
       const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
       const double2 cb = sB[id], rb = sB[id + 1], db = sB[id + SP];
       const double2 opx = sPX[id], opy = sPY[id];
@@ -464,6 +464,17 @@ __device__ __forceinline__ void pd_iterate_cq(int iters, double *sm, int base, i
       // screening test only (not reference arithmetic): fused is fine
       if (fma(p11, p11, p12 * p12) > 0.999999) need |= 1u << (2 * q);
       if (fma(p21, p21, p22 * p22) > 0.999999) need |= 1u << (2 * q + 1);
+    };
+    bool all_d = true, all_p = true;
+#pragma unroll
+    for (int q = 0; q < NP; ++q) all_d = all_d && dual_row[q], all_p = all_p && primal_row[q];
+    if (all_d) {
+#pragma unroll
+      for (int q = 0; q < NP; ++q) dual_px(q);
+    } else {
+#pragma unroll
+      for (int q = 0; q < NP; ++q)
+        if (dual_row[q]) dual_px(q);
     }
     // ---- append saturated pairs: one shared atomic per warp
     int off[2 * NP];
@@ -498,9 +509,7 @@ __device__ __forceinline__ void pd_iterate_cq(int iters, double *sm, int base, i
     }
     __syncthreads();
     // ---- primal descent + TV-L1 shrinkage (:194-208)
-#pragma unroll
-    for (int q = 0; q < NP; ++q) {
-      if (!primal_row[q]) continue;
+    auto primal_px = [&](const int q) {
       const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
       const unsigned f = fl[q];
       const double2 mpx = sPX[id], mpy = sPY[id];
@@ -525,6 +534,14 @@ __device__ __forceinline__ void pd_iterate_cq(int iters, double *sm, int base, i
       sB[id] = make_double2(madx<true>(2.0, n1, -u1[q]), madx<true>(2.0, n2, -u2[q]));
       u1[q] = n1;
       u2[q] = n2;
+    };
+    if (all_p) {
+#pragma unroll
+      for (int q = 0; q < NP; ++q) primal_px(q);
+    } else {
+#pragma unroll
+      for (int q = 0; q < NP; ++q)
+        if (primal_row[q]) primal_px(q);
     }
     __syncthreads();
   }

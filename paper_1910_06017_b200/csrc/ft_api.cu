@@ -1136,7 +1136,7 @@ int ft_tracker_pd_span(ft_tracker *t, double *ms, int *launches, double *pixel_i
   DeviceGuard g(t->ctx->device);
   FT_CUDA_TRY(cudaStreamSynchronize(t->stream));
   double tot = 0.0;
-  for (int wp = 0; wp < t->span.warps; ++wp) {
+  for (int wp = 0; wp < t->span.spans; ++wp) {
     float m = 0.f;
     FT_CUDA_TRY(cudaEventElapsedTime(&m, t->span.ev[2 * wp], t->span.ev[2 * wp + 1]));
     tot += m;

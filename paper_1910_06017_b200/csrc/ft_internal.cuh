@@ -124,9 +124,9 @@ extern PhaseTimer *g_phase;
 // finest-level k_pd_tile launch of every warp.  Captured into the step
 // graph as event-record nodes, so the events hold the most recent replay.
 struct PdSpan {
-  static constexpr int kMaxWarps = 16;
-  cudaEvent_t ev[2 * kMaxWarps] = {};
-  int warps = 0;     // warps recorded in the captured step
+  static constexpr int kMaxSpans = 256;  // (stream group, warp) launch sequences
+  cudaEvent_t ev[2 * kMaxSpans] = {};
+  int spans = 0;     // event pairs recorded in the captured step
   int launches = 0;  // finest-level PD launches between the event pairs
   int64_t pixel_iters = 0;  // pixel-iterations those launches perform (all images)
 };

@@ -1542,62 +1542,80 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
     const PDPlan plan = pd_plan(w, h);
     const bool resident = plan.halo == 0;
     const int halo = plan.halo;
-    for (int wp = 0; wp < p.warps; ++wp) {
-      st = state_ptrs(fw.st[cur], fw.nb, cap);
-      k_warp_setup<<<grid2d(w, h, nb), blk, 0, s>>>(i0, i1, pyr_stride, fw.ix, fw.iy, st.p[U1],
-                                                     st.p[U2], w, h, cap, fw.gx, fw.gy, fw.r0);
-      count_launch();
-      PdSpan *span = lvl == 0 && !resident && wp < PdSpan::kMaxWarps ? g_pd_span : nullptr;
-      if (span) {
-        if (wp == 0) span->warps = span->launches = 0, span->pixel_iters = 0;
-        FT_CUDA_TRY(cudaEventRecordWithFlags(span->ev[2 * wp], s, cudaEventRecordExternal));
-      }
-      int done = 0;
-      while (done < p.iters) {
-        const int n = resident ? p.iters : std::min(halo, p.iters - done);
-        PDArgs a;
-        a.in = state_ptrs(fw.st[cur], fw.nb, cap);
-        a.out = state_ptrs(fw.st[1 - cur], fw.nb, cap);
-        a.gx = fw.gx;
-        a.gy = fw.gy;
-        a.r0 = fw.r0;
-        a.w = w;
-        a.h = h;
-        a.cap = cap;
-        a.halo = halo;
-        a.iters = n;
-        a.first = done == 0;
-        a.nb = nb;
-        a.pow2 = pow2_params(p.tau);
-        a.cone = env_int("FT_PD_CONE", 1);
-        a.cq = env_int("FT_PD_CQ", 1);
-        a.async_ld = env_int("FT_PD_ASYNC", 1);
-        a.tau = p.tau;
-        a.lam = p.lam;
-        a.sigma = sigma;
-        a.shrink = shrink;
-        FT_TRY(pd_launch(plan.cfg, a, nb, s));
+    // Stream groups (FT_PD_GROUP, finest level): a group of streams runs all
+    // of its warps before the next group starts, so the group's state planes
+    // (~63 MB per SD stream incl. ping-pong) can stay resident in the 126 MB
+    // L2 across the PD launches instead of streaming through HBM.
+    const int grp = lvl == 0 ? std::max(1, std::min(nb, env_int("FT_PD_GROUP", nb))) : nb;
+    const int cur0 = cur;
+    PdSpan *span = lvl == 0 && !resident ? g_pd_span : nullptr;
+    if (span) span->spans = span->launches = 0, span->pixel_iters = 0;
+    for (int g0 = 0; g0 < nb; g0 += grp) {
+      const int gn = std::min(grp, nb - g0);
+      cur = cur0;
+      auto sp = [&](int which) {
+        StatePtrs r = state_ptrs(fw.st[which], fw.nb, cap);
+        for (int k = 0; k < NST; ++k) r.p[k] += (int64_t)g0 * cap;
+        return r;
+      };
+      const int64_t go = (int64_t)g0 * cap;
+      const double *gi0 = i0 + (int64_t)g0 * pyr_stride, *gi1 = i1 + (int64_t)g0 * pyr_stride;
+      for (int wp = 0; wp < p.warps; ++wp) {
+        st = sp(cur);
+        k_warp_setup<<<grid2d(w, h, gn), blk, 0, s>>>(gi0, gi1, pyr_stride, fw.ix + go, fw.iy + go,
+                                                       st.p[U1], st.p[U2], w, h, cap, fw.gx + go,
+                                                       fw.gy + go, fw.r0 + go);
+        count_launch();
+        const int si = span && span->spans < PdSpan::kMaxSpans ? span->spans : -1;
+        if (si >= 0)
+          FT_CUDA_TRY(cudaEventRecordWithFlags(span->ev[2 * si], s, cudaEventRecordExternal));
+        int done = 0;
+        while (done < p.iters) {
+          const int n = resident ? p.iters : std::min(halo, p.iters - done);
+          PDArgs a;
+          a.in = sp(cur);
+          a.out = sp(1 - cur);
+          a.gx = fw.gx + go;
+          a.gy = fw.gy + go;
+          a.r0 = fw.r0 + go;
+          a.w = w;
+          a.h = h;
+          a.cap = cap;
+          a.halo = halo;
+          a.iters = n;
+          a.first = done == 0;
+          a.nb = gn;
+          a.pow2 = pow2_params(p.tau);
+          a.cone = env_int("FT_PD_CONE", 1);
+          a.cq = env_int("FT_PD_CQ", 1);
+          a.async_ld = env_int("FT_PD_ASYNC", 1);
+          a.tau = p.tau;
+          a.lam = p.lam;
+          a.sigma = sigma;
+          a.shrink = shrink;
+          FT_TRY(pd_launch(plan.cfg, a, gn, s));
+          cur = 1 - cur;
+          done += n;
+          if (si >= 0) ++span->launches;
+        }
+        if (si >= 0) {
+          FT_CUDA_TRY(cudaEventRecordWithFlags(span->ev[2 * si + 1], s, cudaEventRecordExternal));
+          span->spans = si + 1;
+          span->pixel_iters += (int64_t)w * h * gn * p.iters;
+        }
+        StatePtrs in = sp(cur);
+        StatePtrs out = sp(1 - cur);
+        k_median<<<grid2d(w, h, gn), blk, 0, s>>>(in.p[U1], in.p[U2], out.p[U1], out.p[U2], w, h,
+                                                  cap);
+        count_launch();
         cur = 1 - cur;
-        done += n;
-        if (span) ++span->launches;
-      }
-      if (span) {
-        FT_CUDA_TRY(cudaEventRecordWithFlags(span->ev[2 * wp + 1], s, cudaEventRecordExternal));
-        span->warps = wp + 1;
-        span->pixel_iters += (int64_t)w * h * nb * p.iters;
-      }
-      StatePtrs in = state_ptrs(fw.st[cur], fw.nb, cap);
-      StatePtrs out = state_ptrs(fw.st[1 - cur], fw.nb, cap);
-      k_median<<<grid2d(w, h, nb), blk, 0, s>>>(in.p[U1], in.p[U2], out.p[U1], out.p[U2], w, h,
-                                                cap);
-      count_launch();
-      cur = 1 - cur;
-      if (energy_terms && lvl == 0 && nb == 1) {  // energy_trace (optflow.py:212-213)
-        const int64_t n0 = (int64_t)w * h;
-        StatePtrs now = state_ptrs(fw.st[cur], fw.nb, cap);
-        double *tb = energy_terms + (int64_t)wp * 3 * n0;
-        FT_TRY(launch_energy_terms(i0, i1, now.p[U1], now.p[U2], w, h, p.eps, tb, tb + n0,
-                                   tb + 2 * n0, s));
+        if (energy_terms && lvl == 0 && nb == 1) {  // energy_trace (optflow.py:212-213)
+          const int64_t n0 = (int64_t)w * h;
+          StatePtrs now = sp(cur);
+          double *tb = energy_terms + (int64_t)wp * 3 * n0;
+          FT_TRY(launch_energy_terms(i0, i1, now.p[U1], now.p[U2], w, h, p.eps, tb, tb + n0,
+                                     tb + 2 * n0, s));
+        }
       }
     }
     phase_mark(kLevelNames[lvl < 8 ? lvl : 7]);

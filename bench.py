@@ -147,10 +147,31 @@ def det_records(dets, max_dets):
     return rec, len(dets)
 
 
+def workload(args) -> str:
+    if getattr(args, "flow", "default") == "light":
+        return WORKLOAD.replace("6 scales x 5 warps x 50 iterations",
+                                "6 scales x 2 warps x 10 iterations (SURVEY 8(d) light FlowParams)")
+    return WORKLOAD
+
+
 # ----------------------------------------------------------------------------
 # CPU side: the oracle port of the reference, one SD stream-frame per process
+def _flow_params(flow: str, oracle: bool = False):
+    """default: FlowParams() (the headline C2 workload); light: SURVEY 8(d)'s
+    declared light setting (2 warps x 10 iterations per scale)."""
+    if oracle:
+        from oracle import ftoracle as O
+        cls = O.FlowParams
+    else:
+        from paper_1910_06017_b200.optflow import FlowParams as cls
+    return cls() if flow == "default" else cls(warps_per_level=2, iterations_per_warp=10)
+
+
+FRAME_BYTES = {"default": 22.03e9, "light": 2.52e9}  # SURVEY 8(d) algorithmic bytes / SD frame
+
+
 def _cpu_frame_job(args):
-    rank, s = args
+    rank, s, flow = args
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     from oracle import ftoracle as O
     from paper_1910_06017_b200.synth import make_sequence
@@ -158,20 +179,21 @@ def _cpu_frame_job(args):
                                  scale_change=True)
     st = O.StreamState()
     d0 = [O.Det(d.class_id, d.label, d.score, d.box) for d in dets[0]]
-    O.step(st, frames[0], 0, d0)  # first frame: ST + spawn (not timed)
+    prm = _flow_params(flow, oracle=True)
+    O.step(st, frames[0], 0, d0, prm)  # first frame: ST + spawn (not timed)
     d1 = [O.Det(d.class_id, d.label, d.score, d.box) for d in dets[1]]
     t0 = time.perf_counter()
-    O.step(st, frames[1], 1, d1)  # a full tracked frame: ST + flow + predict + match + update
+    O.step(st, frames[1], 1, d1, prm)  # a full tracked frame: ST + flow + predict + match + update
     return time.perf_counter() - t0
 
 
-def cpu_run(n_procs: int, jobs: int):
+def cpu_run(n_procs: int, jobs: int, flow: str = "default"):
     for var in ("OMP_NUM_THREADS", "MKL_NUM_THREADS", "OPENBLAS_NUM_THREADS"):
         os.environ[var] = "1"  # one core per process (children inherit)
     ctx = mp.get_context("spawn")
     t0 = time.perf_counter()
     with ctx.Pool(n_procs) as pool:
-        per = pool.map(_cpu_frame_job, [(99, s) for s in range(jobs)])
+        per = pool.map(_cpu_frame_job, [(99, s, flow) for s in range(jobs)])
     return time.perf_counter() - t0, per
 
 
@@ -182,14 +204,14 @@ def host_cores() -> int:
         return os.cpu_count() or 1
 
 
-def cpu_baseline_measure():
+def cpu_baseline_measure(flow: str = "default"):
     cores = host_cores()
-    wall, per = cpu_run(cores, cores)
+    wall, per = cpu_run(cores, cores, flow)
     # each process measured its own tracked frame; aggregate = cores / mean
     per_core_fps = 1.0 / float(np.mean(per))
     return {"value": round(per_core_fps * cores, 5), "unit": "frames/s", "cores": cores,
             "kind": "port", "per_core_fps": round(per_core_fps, 5),
-            "sample": f"{cores} processes x 1 tracked SD frame (C2 workload, 100 tracks, default "
+            "sample": f"{cores} processes x 1 tracked SD frame (C2 workload, 100 tracks, {flow} "
                       f"FlowParams) through oracle/ftoracle.py (numpy restatement of the "
                       f"reference, bit-exact); wall {wall:.1f}s"}
 
@@ -201,7 +223,7 @@ def run_reference(args, ws, rank):
     # warm-up: import + a tiny step per process (numpy has no JIT; keeps W semantics)
     step_times = []
     for k in range(args.steps):
-        wall, per = cpu_run(cores, cores)
+        wall, per = cpu_run(cores, cores, args.flow)
         step_times.append(wall)
         if sum(step_times) > args.ref_budget_s:
             break
@@ -212,7 +234,7 @@ def run_reference(args, ws, rank):
             "n_gpus": args.gpus, "steps": steps, "warmup": 0,
             "ms_per_step": round(1000 * wall / steps, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "streams": cores,
+            "config": {"workload": workload(args), "streams": cores,
                        "note": "one step = every host core tracks one SD frame of its own stream; "
                                f"steps capped by a {args.ref_budget_s:.0f}s budget"},
             "cpu_baseline": {"value": round(fps, 5), "unit": "frames/s", "cores": cores,
@@ -245,7 +267,7 @@ def run_ours(args, ws, rank, local):
         for s in range(B):
             dets[t, s], ndets[t, s] = det_records(seqs[s][1][t], max_dets)
 
-    prm = FlowParams()
+    prm = _flow_params(args.flow)
     trk = Tracker(W_, H_, n_streams=B, flow_params=prm, max_tracks=max_tracks, max_dets=max_dets,
                   device=local, motion=args.motion, klt_grid=10)
     stream = torch.cuda.current_stream(dev)
@@ -301,7 +323,7 @@ def run_ours(args, ws, rank, local):
         if tj.get("bytes_per_stream_pixel"):
             traffic = round(tj["bytes_per_stream_pixel"] * B * W_ * H_, 1)
     # step-level roofline: SURVEY 8(d) algorithmic bytes per SD frame (22.03 GB at C2)
-    frame_bytes = 22.03e9
+    frame_bytes = FRAME_BYTES[args.flow]
     step_frac = (value / ws) * frame_bytes / (hbm * 1e9)
 
     # ---------------- end to end through the public API (e2e) ----------------
@@ -331,14 +353,14 @@ def run_ours(args, ws, rank, local):
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_measure()
+        cpu = cpu_baseline_measure(args.flow)
 
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 3), "unit": "frames/s", "n_gpus": ws,
                 "steps": K, "warmup": Wm, "ms_per_step": round(ms_max / K, 4),
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic",
-                "config": {"workload": WORKLOAD, "streams_per_gpu": B, "frame": [W_, H_],
+                "config": {"workload": workload(args), "streams_per_gpu": B, "frame": [W_, H_],
                            "tracks_per_stream": N_OBJ, "parallelism": f"stream-sharded x{ws}",
                            "l2": "working set > L2: every launch streams its state planes "
                                  f"({B} streams x ~70 MB)"},
@@ -385,6 +407,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--motion", choices=["tvl1", "klt"], default="tvl1",
                     help="tvl1: the reference path (headline); klt: SURVEY 8 f4 backend")
+    ap.add_argument("--flow", choices=["default", "light"], default="default",
+                    help="default FlowParams (headline) or SURVEY 8(d)'s light 2 warps x 10 iters")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget-s", type=float, default=150.0)
     args = ap.parse_args()

@@ -641,8 +641,9 @@ struct ft_tracker {
     h_nout = slots[k].nout;
   }
   // graphs keyed by (has_prev, input pointers)
+  int pyr_par = 0;  // which pyramid buffer is current (flips every step)
   struct GraphKey {
-    int has_prev;
+    int has_prev;  // bit 0: has a previous frame; bit 1: pyramid parity
     const void *luma, *dets, *in;
     bool operator<(const GraphKey &o) const {
       if (has_prev != o.has_prev) return has_prev < o.has_prev;
@@ -672,6 +673,10 @@ struct ft_tracker {
   // enqueue one step on `s` reading luma/dets/in from the given device ptrs
   int enqueue(cudaStream_t s, bool has_prev, const uint8_t *luma, const ft_det *dets,
               const int32_t *in, bool host_io) {
+    // pyramid ping-pong: this step builds into `pyr_cur`, the previous step's
+    // pyramid is `pyr_prev` (pyr_par flips after every step; no copy)
+    double *const pyr_cur = pyr_par ? d_pyr_prev : d_pyr_cur;
+    double *const pyr_prev = pyr_par ? d_pyr_cur : d_pyr_prev;
     if (host_io) {
       FT_CUDA_TRY(cudaMemcpyAsync(d_luma, h_luma, (size_t)S * W * H, cudaMemcpyHostToDevice, s));
       FT_CUDA_TRY(cudaMemcpyAsync(d_dets, h_dets, (size_t)S * cfg.max_dets * sizeof(ft_det),
@@ -699,14 +704,14 @@ struct ft_tracker {
     phase_mark("ingest+pyramid");
     if (cfg.motion == FT_MOTION_KLT) {  // SURVEY 8 f4 backend: no ROF, no TV-L1
       KltArgs ka;
-      FT_TRY(build_klt_pyramid(img, P, kgeo, d_pyr_cur, 3 * kgeo.total, S, s, ka.curr));
+      FT_TRY(build_klt_pyramid(img, P, kgeo, pyr_cur, 3 * kgeo.total, S, s, ka.curr));
       phase_mark("klt pyramid");
       const double *kbox = nullptr;
       if (has_prev) {
         ka.prev = ka.curr;
-        ka.prev.lvl = d_pyr_prev;
-        ka.prev.gx = d_pyr_prev + kgeo.total;
-        ka.prev.gy = d_pyr_prev + 2 * kgeo.total;
+        ka.prev.lvl = pyr_prev;
+        ka.prev.gx = pyr_prev + kgeo.total;
+        ka.prev.gy = pyr_prev + 2 * kgeo.total;
         ka.grid = cfg.klt_grid;
         ka.max_pts = cfg.klt_grid * cfg.klt_grid;
         ka.scale = (double)(1 << L);
@@ -718,8 +723,6 @@ struct ft_tracker {
       FT_TRY(launch_tracker_track(T, nullptr, nullptr, P, PW, PH, L, dets, in + 1, in, has_prev,
                                   d_out, d_nout, s, kbox));
       phase_mark("predict+match+update");
-      FT_CUDA_TRY(cudaMemcpyAsync(d_pyr_prev, d_pyr_cur, (size_t)S * 3 * kgeo.total * 8,
-                                  cudaMemcpyDeviceToDevice, s));
       if (host_io) {
         FT_CUDA_TRY(cudaMemcpyAsync(h_out, d_out,
                                     (size_t)S * 2 * cfg.max_tracks * sizeof(ft_track),
@@ -732,22 +735,19 @@ struct ft_tracker {
                                     cfg.rof_iterations, d_st, P, d_rofws, 4 * P, S, s, 0, 0.25));
     phase_mark("structure_texture");
     // (2) flow pyramid of the current ST frame (x255, optflow.py:242-243)
-    FT_TRY(build_flow_pyramid(d_st, P, geo, d_fchain, d_pyr_cur, geo.total, S, s));
+    FT_TRY(build_flow_pyramid(d_st, P, geo, d_fchain, pyr_cur, geo.total, S, s));
     phase_mark("flow pyramid");
     // (3) feature calculation: TV-L1 between previous and current frame
     if (has_prev) {
       FlowParamsD p{cfg.flow.data_weight, cfg.flow.time_step, cfg.flow.huber_epsilon,
                     cfg.flow.warps_per_level, cfg.flow.iterations_per_warp};
-      FT_TRY(run_flow(d_pyr_prev, d_pyr_cur, geo.total, geo.w.data(), geo.h.data(),
+      FT_TRY(run_flow(pyr_prev, pyr_cur, geo.total, geo.w.data(), geo.h.data(),
                       geo.off.data(), scales, p, fw, d_dx, d_dy, P, S, s));
     }
     // (4) prediction, matching, update
     FT_TRY(launch_tracker_track(T, d_dx, d_dy, P, PW, PH, L, dets, in + 1, in, has_prev, d_out,
                                 d_nout, s));
     phase_mark("predict+match+update");
-    // the current pyramid becomes the previous one
-    FT_CUDA_TRY(cudaMemcpyAsync(d_pyr_prev, d_pyr_cur, (size_t)S * geo.total * 8,
-                                cudaMemcpyDeviceToDevice, s));
     if (host_io) {
       FT_CUDA_TRY(cudaMemcpyAsync(h_out, d_out, (size_t)S * 2 * cfg.max_tracks * sizeof(ft_track),
                                   cudaMemcpyDeviceToHost, s));
@@ -768,11 +768,12 @@ struct ft_tracker {
       const int rc = enqueue(s, has_prev, luma, dets, in, host_io);
       g_phase = nullptr;
       timer.report();
+      if (rc == FT_OK) pyr_par ^= 1;
       return rc;
     }
     // host-I/O graphs bake the staging slot's pinned pointers into their
     // copy nodes: key them by those pointers (one graph per slot)
-    GraphKey key{has_prev ? 1 : 0, host_io ? (const void *)h_luma : luma,
+    GraphKey key{(has_prev ? 1 : 0) | (pyr_par << 1), host_io ? (const void *)h_luma : luma,
                  host_io ? (const void *)h_dets : dets, host_io ? (const void *)h_in : in};
     auto it = graphs.find(key);
     if (it == graphs.end()) {
@@ -803,6 +804,7 @@ struct ft_tracker {
     }
     FT_CUDA_TRY(cudaGraphLaunch(it->second.exec, s));
     last_launches = it->second.launches;
+    pyr_par ^= 1;
     return FT_OK;
   }
 };
@@ -947,6 +949,7 @@ int ft_tracker_reset(ft_tracker *t) {
   FT_CUDA_TRY(cudaMemsetAsync(t->d_dy, 0, (size_t)S * t->P * 8, t->stream));
   FT_CUDA_TRY(cudaStreamSynchronize(t->stream));
   t->frames_seen = 0;
+  t->pyr_par = 0;
   return FT_OK;
 }
 

@@ -146,26 +146,45 @@ __device__ __forceinline__ double median9(double *v) {
   return v[4];
 }
 
+__device__ __forceinline__ double med3(double a, double b, double c) {
+  return fmax(fmin(a, b), fmin(fmax(a, b), c));
+}
+
+// Two horizontally adjacent outputs per thread: the four 3-sample columns
+// c-1..c+2 are sorted once and shared; median9 = med3(max of the column
+// minima, med3 of the column medians, min of the column maxima), the same
+// order statistic as the sort (exact selection).
 __global__ void k_median(const double *__restrict__ a1, const double *__restrict__ a2,
                          double *__restrict__ o1, double *__restrict__ o2, int w, int h,
                          int64_t cap) {
   const int64_t so = blockIdx.z * cap;
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
   const int r = blockIdx.y * blockDim.y + threadIdx.y;
   if (r >= h || c >= w) return;
-  int rr[3] = {max(r - 1, 0), r, min(r + 1, h - 1)};
-  int cc[3] = {max(c - 1, 0), c, min(c + 1, w - 1)};
-  double v[9];
+  const int64_t rr[3] = {(int64_t)max(r - 1, 0) * w, (int64_t)r * w, (int64_t)min(r + 1, h - 1) * w};
+  int cc[4];
 #pragma unroll
-  for (int i = 0; i < 3; ++i)
+  for (int k = 0; k < 4; ++k) cc[k] = min(max(c - 1 + k, 0), w - 1);
+  const bool two = c + 1 < w;
 #pragma unroll
-    for (int j = 0; j < 3; ++j) v[i * 3 + j] = a1[so + (int64_t)rr[i] * w + cc[j]];
-  o1[so + (int64_t)r * w + c] = median9(v);
+  for (int f = 0; f < 2; ++f) {
+    const double *a = (f ? a2 : a1) + so;
+    double lo[4], md[4], hi[4];
 #pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int j = 0; j < 3; ++j) v[i * 3 + j] = a2[so + (int64_t)rr[i] * w + cc[j]];
-  o2[so + (int64_t)r * w + c] = median9(v);
+    for (int k = 0; k < 4; ++k) {
+      double x = a[rr[0] + cc[k]], y = a[rr[1] + cc[k]], z = a[rr[2] + cc[k]];
+      cswap(x, y);
+      cswap(y, z);
+      cswap(x, y);
+      lo[k] = x, md[k] = y, hi[k] = z;
+    }
+    double *o = (f ? o2 : o1) + so + (int64_t)r * w + c;
+    o[0] = med3(fmax(fmax(lo[0], lo[1]), lo[2]), med3(md[0], md[1], md[2]),
+                fmin(fmin(hi[0], hi[1]), hi[2]));
+    if (two)
+      o[1] = med3(fmax(fmax(lo[1], lo[2]), lo[3]), med3(md[1], md[2], md[3]),
+                  fmin(fmin(hi[1], hi[2]), hi[3]));
+  }
 }
 
 // Per-pixel terms of the TV-L1 objective (optflow.py:121-137): data term
@@ -1605,8 +1624,8 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
         }
         StatePtrs in = sp(cur);
         StatePtrs out = sp(1 - cur);
-        k_median<<<grid2d(w, h, gn), blk, 0, s>>>(in.p[U1], in.p[U2], out.p[U1], out.p[U2], w, h,
-                                                  cap);
+        k_median<<<grid2d((w + 1) / 2, h, gn), blk, 0, s>>>(in.p[U1], in.p[U2], out.p[U1],
+                                                            out.p[U2], w, h, cap);
         count_launch();
         cur = 1 - cur;
         if (energy_terms && lvl == 0 && nb == 1) {  // energy_trace (optflow.py:212-213)

@@ -28,14 +28,34 @@ __global__ void k_gray8_to_unit(const uint8_t *__restrict__ src, int w, int h, i
   const int64_t n = (int64_t)w * h;
   src += blockIdx.z * ss;
   dst += blockIdx.z * ds;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    dst[i] = (double)src[i] / 255.0;
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t step = (int64_t)gridDim.x * blockDim.x;
+  int64_t done = 0;
+  if (((uintptr_t)src & 7) == 0 && ((uintptr_t)dst & 15) == 0) {
+    // 8 pixels per thread: one 8-byte load, four 16-byte stores
+    const int64_t n8 = n / 8;
+    for (int64_t i = t0; i < n8; i += step) {
+      const uint2 v = reinterpret_cast<const uint2 *>(src)[i];
+      double2 *d = reinterpret_cast<double2 *>(dst + 8 * i);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const unsigned word = k < 2 ? v.x : v.y;
+        const int sh = 16 * (k & 1);
+        d[k] = make_double2((double)((word >> sh) & 0xffu) / 255.0,
+                            (double)((word >> (sh + 8)) & 0xffu) / 255.0);
+      }
+    }
+    done = n8 * 8;
+  }
+  for (int64_t i = done + t0; i < n; i += step) dst[i] = (double)src[i] / 255.0;
 }
 
 // Even-sample output of the separable blur: out(i,j) = sum_k t_k * row_k where
 // row_k = sum_q t_q * src(mirror(2i-2+k), mirror(2j-2+q)); each sum starts at
 // 0.0 and adds taps in order, exactly like smooth_gaussian5's accumulation.
+// Interior columns of an f64 image with 16-byte aligned rows read each input
+// row as three 16-byte loads (columns 2j-2 .. 2j+3; a warp covers 512
+// contiguous bytes per load).
 template <typename T, bool kU8>
 __global__ void k_blur_decimate(const T *__restrict__ src, int w, int h, int64_t ss,
                                 double *__restrict__ dst, int64_t ds,
@@ -45,20 +65,39 @@ __global__ void k_blur_decimate(const T *__restrict__ src, int w, int h, int64_t
   const int i = blockIdx.y * blockDim.y + threadIdx.y;
   if (i >= oh || j >= ow) return;
   src += blockIdx.z * ss;
-  int cols[5];
-#pragma unroll
-  for (int q = 0; q < 5; ++q) cols[q] = mirror(2 * j - 2 + q, w);
   double acc = 0.0;
+  bool vec = false;
+  if constexpr (!kU8)
+    vec = (w % 2 == 0) && ((uintptr_t)src % 16 == 0) && j >= 1 && 2 * j + 3 <= w - 1;
+  if (vec) {
 #pragma unroll
-  for (int k = 0; k < 5; ++k) {
-    const T *row = src + (int64_t)mirror(2 * i - 2 + k, h) * w;
-    double r = 0.0;
-#pragma unroll
-    for (int q = 0; q < 5; ++q) {
-      double v = kU8 ? (double)row[cols[q]] / 255.0 : (double)row[cols[q]];
-      r = r + kTaps[q] * v;
+    for (int k = 0; k < 5; ++k) {
+      const double2 *row =
+          reinterpret_cast<const double2 *>(src + (int64_t)mirror(2 * i - 2 + k, h) * w) + (j - 1);
+      const double2 a = row[0], b = row[1], c = row[2];
+      double r = 0.0;
+      r = r + kTaps[0] * a.x;
+      r = r + kTaps[1] * a.y;
+      r = r + kTaps[2] * b.x;
+      r = r + kTaps[3] * b.y;
+      r = r + kTaps[4] * c.x;
+      acc = acc + kTaps[k] * r;
     }
-    acc = acc + kTaps[k] * r;
+  } else {
+    int cols[5];
+#pragma unroll
+    for (int q = 0; q < 5; ++q) cols[q] = mirror(2 * j - 2 + q, w);
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const T *row = src + (int64_t)mirror(2 * i - 2 + k, h) * w;
+      double r = 0.0;
+#pragma unroll
+      for (int q = 0; q < 5; ++q) {
+        double v = kU8 ? (double)row[cols[q]] / 255.0 : (double)row[cols[q]];
+        r = r + kTaps[q] * v;
+      }
+      acc = acc + kTaps[k] * r;
+    }
   }
   dst[blockIdx.z * ds + (int64_t)i * ow + j] = acc;
   if (dst_scaled) dst_scaled[blockIdx.z * dss + (int64_t)i * ow + j] = acc * scale;
@@ -257,8 +296,9 @@ int grid1d(int64_t n, int bs) {
 
 int launch_gray8_to_unit(const uint8_t *src, int w, int h, int64_t ss, double *dst, int64_t ds,
                          int nb, cudaStream_t s) {
-  k_gray8_to_unit<<<dim3(grid1d((int64_t)w * h, 256), 1, nb), 256, 0, s>>>(src, w, h, ss, dst,
-                                                                           ds);
+  // 8 pixels per thread on the vector path
+  k_gray8_to_unit<<<dim3(grid1d(((int64_t)w * h + 7) / 8, 256), 1, nb), 256, 0, s>>>(src, w, h, ss,
+                                                                                   dst, ds);
   count_launch();
   FT_CUDA_TRY(cudaGetLastError());
   return FT_OK;

@@ -19,8 +19,9 @@ Algorithm (per box, frames at the tracker's processing level L):
 1. a GxG grid: point (i, j) at (x/s + (i+0.5)*w/s/G, y/s + (j+0.5)*h/s/G),
    s = 2^L;
 2. pyramidal LK (Bouguet) prev -> curr over KLT_LEVELS levels built with the
-   same binomial pyramid as the flow path, window (2R+1)^2, central
-   gradients of the source level, up to ITERS Gauss-Newton steps per level
+   same binomial pyramid as the flow path, window (2R+1)^2 sampled with one
+   shared bilinear fraction per window (see `window`), central gradients of
+   the source level, up to ITERS Gauss-Newton steps per level
    (stop when |eta| < EPS_STEP), a point is lost when the structure tensor
    determinant is < MIN_DET or it leaves the level;
 3. the same tracking back curr -> prev; fb = |p_back - p|;
@@ -61,9 +62,37 @@ def sample(img, x, y) -> float:
     return float(O.sample(img, np.array([x]), np.array([y]))[0])
 
 
+_DX = np.array([e % (2 * R + 1) - R for e in range((2 * R + 1) ** 2)])
+_DY = np.array([e // (2 * R + 1) - R for e in range((2 * R + 1) ** 2)])
+
+
+def window(img: np.ndarray, qx: float, qy: float):
+    """The (2R+1)^2 window samples around (qx, qy), element e at integer offset
+    (e % (2R+1) - R, e // (2R+1) - R): the centre is clamped to the image,
+    split into an integer base and a fraction shared by the whole window
+    (standard KLT interpolation), and every sample is the bilinear blend of
+    the four border-replicated neighbours of base + offset:
+    top = a00*(1-fx) + a01*fx, bot = a10*(1-fx) + a11*fx,
+    v = top*(1-fy) + bot*fy."""
+    h, w = img.shape
+    qx = qx if qx > 0.0 else 0.0       # comparison order of the device clamp
+    qx = qx if qx < w - 1.0 else w - 1.0
+    qy = qy if qy > 0.0 else 0.0
+    qy = qy if qy < h - 1.0 else h - 1.0
+    x0, y0 = math.floor(qx), math.floor(qy)
+    fx, fy = qx - x0, qy - y0
+    gx, gy = 1.0 - fx, 1.0 - fy
+    c0 = np.clip(x0 + _DX, 0, w - 1)
+    c1 = np.clip(x0 + _DX + 1, 0, w - 1)
+    r0 = np.clip(y0 + _DY, 0, h - 1)
+    r1 = np.clip(y0 + _DY + 1, 0, h - 1)
+    top = img[r0, c0] * gx + img[r0, c1] * fx
+    bot = img[r1, c0] * gx + img[r1, c1] * fx
+    return (top * gy + bot * fy).tolist()
+
+
 def lk_track(src_pyr, src_grad, dst_pyr, px: float, py: float):
     """Pyramidal LK of one point; returns (x, y, ok) at level 0 coordinates."""
-    offs = [(dx, dy) for dy in range(-R, R + 1) for dx in range(-R, R + 1)]
     gx_, gy_ = 0.0, 0.0
     ok = True
     for lvl in range(KLT_LEVELS - 1, -1, -1):
@@ -75,11 +104,9 @@ def lk_track(src_pyr, src_grad, dst_pyr, px: float, py: float):
         if not (0.0 <= cx <= w - 1.0 and 0.0 <= cy <= h - 1.0):
             ok = False
             break
-        wx = np.array([cx + dx for dx, _ in offs])
-        wy = np.array([cy + dy for _, dy in offs])
-        ixs = O.sample(Ix, wx, wy).tolist()   # elementwise: same bits as one-by-one
-        iys = O.sample(Iy, wx, wy).tolist()
-        ivs = O.sample(I, wx, wy).tolist()
+        ixs = window(Ix, cx, cy)
+        iys = window(Iy, cx, cy)
+        ivs = window(I, cx, cy)
         gxx = lane_sum([a * a for a in ixs])
         gxy = lane_sum([a * b for a, b in zip(ixs, iys)])
         gyy = lane_sum([b * b for b in iys])
@@ -90,8 +117,7 @@ def lk_track(src_pyr, src_grad, dst_pyr, px: float, py: float):
         vx, vy = 0.0, 0.0
         for _ in range(ITERS):
             qx, qy = cx + gx_ + vx, cy + gy_ + vy
-            jv = O.sample(J, np.array([qx + dx for dx, _ in offs]),
-                          np.array([qy + dy for _, dy in offs])).tolist()
+            jv = window(J, qx, qy)
             dI = [iv - jj for iv, jj in zip(ivs, jv)]
             bx = lane_sum([d * a for d, a in zip(dI, ixs)])
             by = lane_sum([d * b for d, b in zip(dI, iys)])

@@ -23,6 +23,47 @@ __device__ __forceinline__ double warp_sum(double part) {
   return part;
 }
 
+// Window sampling (klt_oracle.window): the centre is clamped to the image and
+// split into an integer base and one bilinear fraction shared by the whole
+// window; element e samples base + (e % 9 - 4, e / 9 - 4) with
+// border-replicated neighbours.  Per-lane element offsets are precomputed.
+struct WinPos {
+  int x0, y0;
+  double fx, fy, gx, gy;  // fraction and 1 - fraction
+  bool inside;            // every tap of the window lies in the image
+};
+
+__device__ __forceinline__ WinPos win_pos(double qx, double qy, int w, int h) {
+  WinPos p;
+  qx = qx > 0.0 ? qx : 0.0;
+  qx = qx < w - 1.0 ? qx : w - 1.0;
+  qy = qy > 0.0 ? qy : 0.0;
+  qy = qy < h - 1.0 ? qy : h - 1.0;
+  p.x0 = (int)floor(qx);
+  p.y0 = (int)floor(qy);
+  p.fx = qx - (double)p.x0;
+  p.fy = qy - (double)p.y0;
+  p.gx = 1.0 - p.fx;
+  p.gy = 1.0 - p.fy;
+  p.inside = p.x0 - kR >= 0 && p.x0 + kR + 1 <= w - 1 && p.y0 - kR >= 0 && p.y0 + kR + 1 <= h - 1;
+  return p;
+}
+
+__device__ __forceinline__ double win_sample(const double *__restrict__ img, int w, int h,
+                                             const WinPos &p, int dx, int dy) {
+  int c0 = p.x0 + dx, r0 = p.y0 + dy, c1 = c0 + 1, r1 = r0 + 1;
+  if (!p.inside) {
+    c0 = min(max(c0, 0), w - 1);
+    c1 = min(max(c1, 0), w - 1);
+    r0 = min(max(r0, 0), h - 1);
+    r1 = min(max(r1, 0), h - 1);
+  }
+  const double *a = img + (int64_t)r0 * w, *b = img + (int64_t)r1 * w;
+  const double top = a[c0] * p.gx + a[c1] * p.fx;
+  const double bot = b[c0] * p.gx + b[c1] * p.fx;
+  return top * p.gy + bot * p.fy;
+}
+
 // Pyramidal LK of one point from pyramid A to pyramid B (image `img`);
 // identical on every lane of the warp.  Returns false when the point is lost.
 __device__ bool lk_point(const KltPyr &A, const KltPyr &B, int img, double px, double py,
@@ -42,17 +83,19 @@ __device__ bool lk_point(const KltPyr &A, const KltPyr &B, int img, double px, d
       break;
     }
     double ix[kPerLane], iy[kPerLane], iv[kPerLane];
+    int ox[kPerLane], oy[kPerLane];
     double pxx = 0.0, pxy = 0.0, pyy = 0.0;
+    const WinPos pc = win_pos(cx, cy, w, h);
 #pragma unroll
     for (int k = 0; k < kPerLane; ++k) {
       const int e = lane + 32 * k;
+      ox[k] = e % (2 * kR + 1) - kR;
+      oy[k] = e / (2 * kR + 1) - kR;
       ix[k] = iy[k] = iv[k] = 0.0;
       if (e < kWin) {
-        const double wx = cx + (double)(e % (2 * kR + 1) - kR);
-        const double wy = cy + (double)(e / (2 * kR + 1) - kR);
-        ix[k] = ft_bsample(Ix, w, h, wx, wy);
-        iy[k] = ft_bsample(Iy, w, h, wx, wy);
-        iv[k] = ft_bsample(I, w, h, wx, wy);
+        ix[k] = win_sample(Ix, w, h, pc, ox[k], oy[k]);
+        iy[k] = win_sample(Iy, w, h, pc, ox[k], oy[k]);
+        iv[k] = win_sample(I, w, h, pc, ox[k], oy[k]);
         pxx = pxx + ix[k] * ix[k];
         pxy = pxy + ix[k] * iy[k];
         pyy = pyy + iy[k] * iy[k];
@@ -67,13 +110,13 @@ __device__ bool lk_point(const KltPyr &A, const KltPyr &B, int img, double px, d
     double vx = 0.0, vy = 0.0;
     for (int it = 0; it < kKltIters; ++it) {
       const double qx_ = cx + ga + vx, qy_ = cy + gb + vy;
+      const WinPos pq = win_pos(qx_, qy_, w, h);
       double bxp = 0.0, byp = 0.0;
 #pragma unroll
       for (int k = 0; k < kPerLane; ++k) {
         const int e = lane + 32 * k;
         if (e < kWin) {
-          const double jv = ft_bsample(J, w, h, qx_ + (double)(e % (2 * kR + 1) - kR),
-                                       qy_ + (double)(e / (2 * kR + 1) - kR));
+          const double jv = win_sample(J, w, h, pq, ox[k], oy[k]);
           const double dI = iv[k] - jv;
           bxp = bxp + dI * ix[k];
           byp = byp + dI * iy[k];

@@ -64,6 +64,20 @@ __device__ __forceinline__ double win_sample(const double *__restrict__ img, int
   return top * p.gy + bot * p.fy;
 }
 
+// Two lane-strided partial sums reduced at once, bit-identical to two
+// warp_sum butterflies: at offset 16 lanes < 16 keep the first sum and
+// lanes >= 16 the second (each adds its partner's partial exactly as the
+// butterfly does), the remaining offsets stay within a half, and the totals
+// are read from lanes 0 and 16.
+__device__ __forceinline__ void warp_sum2(double a, double b, double &sa, double &sb) {
+  const bool lo = (threadIdx.x & 16) == 0;
+  double v = (lo ? a : b) + __shfl_xor_sync(0xffffffffu, lo ? b : a, 16);
+#pragma unroll
+  for (int off = 8; off > 0; off >>= 1) v = v + __shfl_xor_sync(0xffffffffu, v, off);
+  sa = __shfl_sync(0xffffffffu, v, 0);
+  sb = __shfl_sync(0xffffffffu, v, 16);
+}
+
 // Pyramidal LK of one point from pyramid A to pyramid B (image `img`);
 // identical on every lane of the warp.  Returns false when the point is lost.
 __device__ bool lk_point(const KltPyr &A, const KltPyr &B, int img, double px, double py,
@@ -101,7 +115,9 @@ __device__ bool lk_point(const KltPyr &A, const KltPyr &B, int img, double px, d
         pyy = pyy + iy[k] * iy[k];
       }
     }
-    const double gxx = warp_sum(pxx), gxy = warp_sum(pxy), gyy = warp_sum(pyy);
+    double gxx, gxy;
+    warp_sum2(pxx, pxy, gxx, gxy);
+    const double gyy = warp_sum(pyy);
     const double det = gxx * gyy - gxy * gxy;
     if (!(det >= kKltMinDet)) {
       ok = false;
@@ -122,7 +138,8 @@ __device__ bool lk_point(const KltPyr &A, const KltPyr &B, int img, double px, d
           byp = byp + dI * iy[k];
         }
       }
-      const double bx = warp_sum(bxp), by = warp_sum(byp);
+      double bx, by;
+      warp_sum2(bxp, byp, bx, by);
       const double ex = (gyy * bx - gxy * by) / det;
       const double ey = (gxx * by - gxy * bx) / det;
       vx = vx + ex;

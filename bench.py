@@ -389,7 +389,8 @@ def run_ours(args, ws, rank, local):
             line["config"]["workload"] = (
                 "C2 with the KLT/MedianFlow backend (SURVEY 8 f4): 720x576 SD, 100 tracks, "
                 "10x10 points/box, 3-level LK pyramid, 9x9 window, forward-backward check, fp64")
-            line["config"]["l2"] = "per-stream KLT pyramids (~10 MB) re-read per step"
+            line["config"]["l2"] = (f"working set > L2: {B} streams x ~26 MB of KLT pyramids "
+                                     "(prev + cur) per step")
             line["roofline"] = None  # gather-latency bound; no streaming-roofline model
             line["step_roofline_frac"] = None
         print(json.dumps(line), flush=True)

@@ -19,3 +19,7 @@ KCMD="python bench.py --motion klt --no-cpu-baseline"
 $KCMD > gpurun_out/kplain.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:k_klt_points -s 2 -c 1 \
     -o gpurun_out/klt_full $KCMD > gpurun_out/ncu_klt.log 2>&1; echo "klt full rc=$?"
+python bench.py --flow light > gpurun_out/bench_light.log 2>&1; echo "light rc=$?"
+python bench.py --flow light --impl reference > gpurun_out/bench_light_ref.log 2>&1; echo "light ref rc=$?"
+bash tools/gpu_pyr_profile.sh
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"

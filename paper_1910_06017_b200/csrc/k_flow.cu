@@ -250,6 +250,13 @@ struct PDArgs {
   int cone;  // compute only the rows feeding the written interior (FT_PD_CONE)
   int cq;    // CTA-wide projection queue (FT_PD_CQ)
   int async_ld;  // exchange planes loaded with cp.async (FT_PD_ASYNC)
+  // k_pd_tile half-step schedule: the launch runs `nhalf` alternating dual (D)
+  // / primal (P) half-steps, starting with D when `first` (u-bar = u, p = 0)
+  // and with P otherwise; it ends after a D (state u, p) unless `last` (ends
+  // after a P, writes u only).  rows_lo/hi[j]: rows half-step j must compute
+  // (shrinking cone; cone_rows == 0 -> all rows).
+  int nhalf, last, cone_rows;
+  signed char rows_lo[16], rows_hi[16];
   double tau, lam, sigma, shrink;  // shrink = 1/(1+sigma*eps)
 };
 
@@ -430,137 +437,145 @@ __device__ __forceinline__ void pd_iterate(int iters, double *sm, int base, int 
   }
 }
 
-// Same iteration with a CTA-wide projection queue (k_pd_tile): the dual step
-// stores its unprojected p, the saturated pairs of the whole CTA (~9 % of
-// pairs at C2) are appended to one shared index list, and after a barrier
-// the first ceil(n/32) warps project them in place -- instead of every warp
-// running the hypot + division code for its own ~4 saturated pairs with most
-// lanes idle.  The primal step re-reads its own p from shared memory, so p
-// is not held in registers across the barriers.  Bit-identical to
-// pd_iterate: the same pairs get the same max(1, hypot) and divisions.
+// Half-step schedule of k_pd_tile with a CTA-wide projection queue.
+//
+// The launch boundary sits after a dual step, where the state is (u, p):
+// u-bar is recomputed by the primal step that opens the next launch, so a
+// launch reads 9 planes and writes 6 instead of 11 / 8.
+//
+// Dual half-step: the unprojected p is stored in place, the saturated pairs
+// of the whole CTA (~9 % at C2) are appended to one shared index list, and
+// after a barrier the first ceil(n/32) warps project them in place (instead
+// of every warp running the hypot + division code for its own ~4 pairs with
+// most lanes idle).  Primal half-step: reads its p from shared memory.
+// Same arithmetic in the same order as the reference iteration.
 template <int TW, int BY, int PY, bool P2, bool IN>
-__device__ __forceinline__ void pd_iterate_cq(int iters, double *sm, int base, int tx, int ty,
-                                              const unsigned *fl, double *u1, double *u2,
-                                              const double *gx, const double *gy,
-                                              const double *r0, const double *thr,
-                                              const double *ig2, double tau, double tl,
-                                              double sigma, double shrink, int *qidx, int *ctr,
-                                              int cone) {
+__device__ __forceinline__ void pd_halfsteps_cq(const PDArgs &a, double *sm, int base, int tx,
+                                                int ty, const unsigned *fl, double *u1,
+                                                double *u2, const double *gx, const double *gy,
+                                                const double *r0, const double *thr,
+                                                const double *ig2, double tl, int *qidx,
+                                                int *ctr) {
   using G = PDGeom<TW, BY, PY>;
   constexpr int NX = G::NX, NP = G::NP, SP = G::SP, PL = G::PLANE, TH = G::TH;
   constexpr int NT = 32 * BY;
+  const double tau = a.tau, sigma = a.sigma, shrink = a.shrink;
   double2 *const sB = reinterpret_cast<double2 *>(sm), *const sPX = sB + PL, *const sPY = sPX + PL;
   double *const dPX = reinterpret_cast<double *>(sPX), *const dPY = reinterpret_cast<double *>(sPY);
   const unsigned lt_mask = (1u << tx) - 1u;
   const int tid = ty * 32 + tx;
-  for (int it = 0; it < iters; ++it) {
-    bool dual_row[NP], primal_row[NP];
+  int nd = 0;  // dual half-steps done (queue counter parity)
+  for (int j = 0; j < a.nhalf; ++j) {
+    const bool dual = ((j & 1) == 0) == (a.first != 0);
+    const int lo = a.cone_rows ? a.rows_lo[j] : 0, hi = a.cone_rows ? a.rows_hi[j] : TH;
+    bool row_on[NP];
+    bool all = true;
 #pragma unroll
-    for (int q = 0; q < NP; ++q) {  // shrinking cone, as in pd_iterate
+    for (int q = 0; q < NP; ++q) {
       const int lr = ty + BY * (q / NX);
-      dual_row[q] = cone < 0 || (lr >= cone + it && lr < TH - 1 - cone - it);
-      primal_row[q] = cone < 0 || (lr >= cone + it + 1 && lr < TH - 1 - cone - it);
+      row_on[q] = lr >= lo && lr < hi;
+      all = all && row_on[q];
     }
-    // ---- dual ascent with Huber prox (:180-185), unprojected p stored in place
-    unsigned need = 0;
-    // (the common all-rows-active case runs branch-free so the compiler can
-    // interleave the pixels' dependency chains)
-    auto dual_px = [&](const int q) {
-      const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
-      const double2 cb = sB[id], rb = sB[id + 1], db = sB[id + SP];
-      const double2 opx = sPX[id], opy = sPY[id];
-      const bool R = IN || (fl[q] & FL_R), D = IN || (fl[q] & FL_D);
-      const double a1x = R ? rb.x - cb.x : 0.0;
-      const double a1y = D ? db.x - cb.x : 0.0;
-      const double a2x = R ? rb.y - cb.y : 0.0;
-      const double a2y = D ? db.y - cb.y : 0.0;
-      const double p11 = madx<P2>(sigma, a1x, opx.x) * shrink;
-      const double p12 = madx<P2>(sigma, a1y, opy.x) * shrink;
-      const double p21 = madx<P2>(sigma, a2x, opx.y) * shrink;
-      const double p22 = madx<P2>(sigma, a2y, opy.y) * shrink;
-      sPX[id] = make_double2(p11, p21);
-      sPY[id] = make_double2(p12, p22);
-      // screening test only (not reference arithmetic): fused is fine
-      if (fma(p11, p11, p12 * p12) > 0.999999) need |= 1u << (2 * q);
-      if (fma(p21, p21, p22 * p22) > 0.999999) need |= 1u << (2 * q + 1);
-    };
-    bool all_d = true, all_p = true;
-#pragma unroll
-    for (int q = 0; q < NP; ++q) all_d = all_d && dual_row[q], all_p = all_p && primal_row[q];
-    if (all_d) {
-#pragma unroll
-      for (int q = 0; q < NP; ++q) dual_px(q);
-    } else {
-#pragma unroll
-      for (int q = 0; q < NP; ++q)
-        if (dual_row[q]) dual_px(q);
-    }
-    // ---- append saturated pairs: one shared atomic per warp
-    int off[2 * NP];
-    int total = 0;
-    if (__any_sync(0xffffffffu, need != 0u)) {
-#pragma unroll
-      for (int j = 0; j < 2 * NP; ++j) {
-        const unsigned m = __ballot_sync(0xffffffffu, (need >> j) & 1u);
-        off[j] = total + __popc(m & lt_mask);
-        total += __popc(m);
-      }
-      int wbase = 0;
-      if (tx == 0) wbase = atomicAdd(&ctr[it & 1], total);
-      wbase = __shfl_sync(0xffffffffu, wbase, 0);
-#pragma unroll
-      for (int j = 0; j < 2 * NP; ++j) {
-        const int q = j >> 1;
+    if (dual) {
+      // ---- dual ascent with Huber prox (:180-185), unprojected p stored in place
+      unsigned need = 0;
+      // (the common all-rows-active case runs branch-free so the compiler can
+      // interleave the pixels' dependency chains)
+      auto dual_px = [&](const int q) {
         const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
-        if ((need >> j) & 1u) qidx[wbase + off[j]] = 2 * id + (j & 1);
+        const double2 cb = sB[id], rb = sB[id + 1], db = sB[id + SP];
+        const double2 opx = sPX[id], opy = sPY[id];
+        const bool R = IN || (fl[q] & FL_R), D = IN || (fl[q] & FL_D);
+        const double a1x = R ? rb.x - cb.x : 0.0;
+        const double a1y = D ? db.x - cb.x : 0.0;
+        const double a2x = R ? rb.y - cb.y : 0.0;
+        const double a2y = D ? db.y - cb.y : 0.0;
+        const double p11 = madx<P2>(sigma, a1x, opx.x) * shrink;
+        const double p12 = madx<P2>(sigma, a1y, opy.x) * shrink;
+        const double p21 = madx<P2>(sigma, a2x, opx.y) * shrink;
+        const double p22 = madx<P2>(sigma, a2y, opy.y) * shrink;
+        sPX[id] = make_double2(p11, p21);
+        sPY[id] = make_double2(p12, p22);
+        // screening test only (not reference arithmetic): fused is fine
+        if (fma(p11, p11, p12 * p12) > 0.999999) need |= 1u << (2 * q);
+        if (fma(p21, p21, p22 * p22) > 0.999999) need |= 1u << (2 * q + 1);
+      };
+      if (all) {
+#pragma unroll
+        for (int q = 0; q < NP; ++q) dual_px(q);
+      } else {
+#pragma unroll
+        for (int q = 0; q < NP; ++q)
+          if (row_on[q]) dual_px(q);
       }
-    }
-    __syncthreads();
-    // ---- unit-ball projection n = max(1, hypot(.)); p /= n (:186-191)
-    const int n = ctr[it & 1];
-    if (tid == 0) ctr[(it + 1) & 1] = 0;  // next iteration's list (unused until then)
-    for (int e = tid; e < n; e += NT) {
-      const int k = qidx[e];
-      const double a = dPX[k], b = dPY[k];
-      const double nn = np_max(1.0, glibc_hypot(a, b));
-      dPX[k] = a / nn;
-      dPY[k] = b / nn;
-    }
-    __syncthreads();
-    // ---- primal descent + TV-L1 shrinkage (:194-208)
-    auto primal_px = [&](const int q) {
-      const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
-      const unsigned f = fl[q];
-      const double2 mpx = sPX[id], mpy = sPY[id];
-      const double p11 = mpx.x, p21 = mpx.y, p12 = mpy.x, p22 = mpy.y;
-      const double2 lp = sPX[id - 1], up = sPY[id - SP];
-      const double l11 = lp.x, l21 = lp.y, u12 = up.x, u22 = up.y;
-      const bool L = IN || (f & FL_L), LC = !IN && (f & FL_LASTC);
-      const bool U = IN || (f & FL_U), LR = !IN && (f & FL_LASTR);
-      const double dx1 = L ? (LC ? -l11 : p11 - l11) : p11;
-      const double dx2 = L ? (LC ? -l21 : p21 - l21) : p21;
-      const double dy1 = U ? (LR ? -u12 : p12 - u12) : p12;
-      const double dy2 = U ? (LR ? -u22 : p22 - u22) : p22;
-      const double v1 = madx<P2>(tau, dx1 + dy1, u1[q]);
-      const double v2 = madx<P2>(tau, dx2 + dy2, u2[q]);
-      const double rho = r0[q] + gx[q] * v1 + gy[q] * v2;
-      const bool lo = rho < -thr[q];
-      const bool hi = rho > thr[q];
-      double d = lo ? tl : (hi ? -tl : -rho * ig2[q]);
-      d = (ig2[q] != 0.0 || lo || hi) ? d : 0.0;  // ig2 != 0 <=> |grad|^2 > 1e-12
-      const double n1 = v1 + d * gx[q];
-      const double n2 = v2 + d * gy[q];
-      sB[id] = make_double2(madx<true>(2.0, n1, -u1[q]), madx<true>(2.0, n2, -u2[q]));
-      u1[q] = n1;
-      u2[q] = n2;
-    };
-    if (all_p) {
+      // ---- append saturated pairs: one shared atomic per warp
+      int off[2 * NP];
+      int total = 0;
+      if (__any_sync(0xffffffffu, need != 0u)) {
 #pragma unroll
-      for (int q = 0; q < NP; ++q) primal_px(q);
+        for (int k = 0; k < 2 * NP; ++k) {
+          const unsigned m = __ballot_sync(0xffffffffu, (need >> k) & 1u);
+          off[k] = total + __popc(m & lt_mask);
+          total += __popc(m);
+        }
+        int wbase = 0;
+        if (tx == 0) wbase = atomicAdd(&ctr[nd & 1], total);
+        wbase = __shfl_sync(0xffffffffu, wbase, 0);
+#pragma unroll
+        for (int k = 0; k < 2 * NP; ++k) {
+          const int q = k >> 1;
+          const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
+          if ((need >> k) & 1u) qidx[wbase + off[k]] = 2 * id + (k & 1);
+        }
+      }
+      __syncthreads();
+      // ---- unit-ball projection n = max(1, hypot(.)); p /= n (:186-191)
+      const int n = ctr[nd & 1];
+      if (tid == 0) ctr[(nd + 1) & 1] = 0;  // next dual's list (unused until then)
+      for (int e = tid; e < n; e += NT) {
+        const int k = qidx[e];
+        const double pa = dPX[k], pb = dPY[k];
+        const double nn = np_max(1.0, glibc_hypot(pa, pb));
+        dPX[k] = pa / nn;
+        dPY[k] = pb / nn;
+      }
+      ++nd;
     } else {
+      // ---- primal descent + TV-L1 shrinkage (:194-208), u-bar stored in place
+      auto primal_px = [&](const int q) {
+        const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
+        const unsigned f = fl[q];
+        const double2 mpx = sPX[id], mpy = sPY[id];
+        const double p11 = mpx.x, p21 = mpx.y, p12 = mpy.x, p22 = mpy.y;
+        const double2 lp = sPX[id - 1], up = sPY[id - SP];
+        const double l11 = lp.x, l21 = lp.y, u12 = up.x, u22 = up.y;
+        const bool L = IN || (f & FL_L), LC = !IN && (f & FL_LASTC);
+        const bool U = IN || (f & FL_U), LR = !IN && (f & FL_LASTR);
+        const double dx1 = L ? (LC ? -l11 : p11 - l11) : p11;
+        const double dx2 = L ? (LC ? -l21 : p21 - l21) : p21;
+        const double dy1 = U ? (LR ? -u12 : p12 - u12) : p12;
+        const double dy2 = U ? (LR ? -u22 : p22 - u22) : p22;
+        const double v1 = madx<P2>(tau, dx1 + dy1, u1[q]);
+        const double v2 = madx<P2>(tau, dx2 + dy2, u2[q]);
+        const double rho = r0[q] + gx[q] * v1 + gy[q] * v2;
+        const bool lo_ = rho < -thr[q];
+        const bool hi_ = rho > thr[q];
+        double d = lo_ ? tl : (hi_ ? -tl : -rho * ig2[q]);
+        d = (ig2[q] != 0.0 || lo_ || hi_) ? d : 0.0;  // ig2 != 0 <=> |grad|^2 > 1e-12
+        const double n1 = v1 + d * gx[q];
+        const double n2 = v2 + d * gy[q];
+        sB[id] = make_double2(madx<true>(2.0, n1, -u1[q]), madx<true>(2.0, n2, -u2[q]));
+        u1[q] = n1;
+        u2[q] = n2;
+      };
+      if (all) {
 #pragma unroll
-      for (int q = 0; q < NP; ++q)
-        if (primal_row[q]) primal_px(q);
+        for (int q = 0; q < NP; ++q) primal_px(q);
+      } else {
+#pragma unroll
+        for (int q = 0; q < NP; ++q)
+          if (row_on[q]) primal_px(q);
+      }
     }
     __syncthreads();
   }
@@ -622,30 +637,19 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const PDArgs a) {
       const bool in = gc >= 0 && gc < W && gr >= 0 && gr < H;
       const int64_t o = so + (int64_t)gr * W + gc;
       const int id = base + k * BY * SP + 32 * cx;
-      // exchange planes go straight to shared memory (cp.async, zero-filled
-      // outside the image): no registers held, all copies in flight at once
-      const bool async_x = a.async_ld && !a.first;
-      if (async_x) {
+      // p planes go straight to shared memory (cp.async, zero-filled outside
+      // the image): no registers held, all copies in flight at once.  u-bar
+      // is not part of the state between launches: the launch opens with a
+      // primal half-step that writes it (first launch: u-bar = u, p = 0).
+      if (!a.first) {
 #pragma unroll
-        for (int f = 0; f < 6; ++f)
+        for (int f = 2; f < 6; ++f)
           cp_async8(&sm[sxi(f, id, PL)], in ? a.in.p[B1 + f] + o : a.in.p[B1 + f], in);
       }
-      double vu1 = 0, vu2 = 0, vb1 = 0, vb2 = 0, q11 = 0, q12 = 0, q21 = 0, q22 = 0;
-      double vgx = 0, vgy = 0, vr0 = 0;
+      double vu1 = 0, vu2 = 0, vgx = 0, vgy = 0, vr0 = 0;
       if (in) {
         vu1 = a.in.p[U1][o];
         vu2 = a.in.p[U2][o];
-        if (a.first) {
-          vb1 = vu1;  // ub = u, p = 0 at the start of a warp (optflow.py:169-174)
-          vb2 = vu2;
-        } else if (!async_x) {
-          vb1 = a.in.p[B1][o];
-          vb2 = a.in.p[B2][o];
-          q11 = a.in.p[P11][o];
-          q12 = a.in.p[P12][o];
-          q21 = a.in.p[P21][o];
-          q22 = a.in.p[P22][o];
-        }
         vgx = a.gx[o];
         vgy = a.gy[o];
         vr0 = a.r0[o];
@@ -662,41 +666,26 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const PDArgs a) {
       fl[q] = (gc < W - 1 ? FL_R : 0u) | (gr < H - 1 ? FL_D : 0u) | (gc > 0 ? FL_L : 0u) |
               (gc == W - 1 ? FL_LASTC : 0u) | (gr > 0 ? FL_U : 0u) | (gr == H - 1 ? FL_LASTR : 0u) |
               (ok ? FL_OK : 0u);
-      if (!async_x) {
-        sm[sxi(0, id, PL)] = vb1;
-        sm[sxi(1, id, PL)] = vb2;
-        sm[sxi(2, id, PL)] = q11;
-        sm[sxi(3, id, PL)] = q12;
-        sm[sxi(4, id, PL)] = q21;
-        sm[sxi(5, id, PL)] = q22;
+      if (a.first) {  // ub = u, p = 0 at the start of a warp (optflow.py:169-174)
+        sm[sxi(0, id, PL)] = vu1;
+        sm[sxi(1, id, PL)] = vu2;
+#pragma unroll
+        for (int f = 2; f < 6; ++f) sm[sxi(f, id, PL)] = 0.0;
       }
     }
   }
-  if (a.async_ld && !a.first) cp_async_wait_all();
+  if (!a.first) cp_async_wait_all();
   if (tid < 2) reinterpret_cast<int *>(sm + 6 * PL)[2 * NP * 32 * BY + tid] = 0;  // queue counters
   __syncthreads();
 
-  double2 *const queue = reinterpret_cast<double2 *>(sm + 6 * PL) + ty * (2 * NP * 32);
-  BlockBarrier bar;
   // tile free of image-border pixels (uniform per CTA): flag-free fast path
   const bool interior = ox >= 1 && oy >= 1 && ox + TW <= W - 1 && oy + TH <= H - 1;
-  const int cone = a.cone && a.halo > 0 && a.iters <= a.halo ? a.halo - a.iters : -1;
-  if (a.cq) {
+  {
     int *const qidx = reinterpret_cast<int *>(sm + 6 * PL);
     int *const ctr = qidx + 2 * NP * 32 * BY;
-#define FT_PD_CALL(P2_, IN_)                                                                  \
-  pd_iterate_cq<TW, BY, PY, P2_, IN_>(a.iters, sm, base, tx, ty, fl, u1, u2, gx, gy, r0, thr, \
-                                      ig2, a.tau, tl, a.sigma, a.shrink, qidx, ctr, cone)
-    if (a.pow2) {
-      if (interior) FT_PD_CALL(true, true); else FT_PD_CALL(true, false);
-    } else {
-      if (interior) FT_PD_CALL(false, true); else FT_PD_CALL(false, false);
-    }
-#undef FT_PD_CALL
-  } else {
-#define FT_PD_CALL(P2_, IN_)                                                                  \
-  pd_iterate<TW, BY, PY, P2_, IN_>(a.iters, sm, base, tx, fl, u1, u2, gx, gy, r0, thr, ig2,   \
-                                   a.tau, tl, a.sigma, a.shrink, queue, bar, ty, cone)
+#define FT_PD_CALL(P2_, IN_)                                                                 \
+  pd_halfsteps_cq<TW, BY, PY, P2_, IN_>(a, sm, base, tx, ty, fl, u1, u2, gx, gy, r0, thr, ig2, \
+                                        tl, qidx, ctr)
     if (a.pow2) {
       if (interior) FT_PD_CALL(true, true); else FT_PD_CALL(true, false);
     } else {
@@ -705,7 +694,8 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const PDArgs a) {
 #undef FT_PD_CALL
   }
 
-  // ---- write back the exact interior
+  // ---- write back the exact interior: u, and p unless this is the warp's
+  // last launch (the next warp starts from p = 0)
   const int lo_x = a.halo, hi_x = TW - a.halo;
   const int lo_y = a.halo, hi_y = TH - a.halo;
 #pragma unroll
@@ -719,8 +709,10 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const PDArgs a) {
     const int64_t o = so + (int64_t)gr * W + gc;
     a.out.p[U1][o] = u1[q];
     a.out.p[U2][o] = u2[q];
+    if (!a.last) {
 #pragma unroll
-    for (int f = 0; f < 6; ++f) a.out.p[B1 + f][o] = sm[sxi(f, id, PL)];
+      for (int f = 2; f < 6; ++f) a.out.p[B1 + f][o] = sm[sxi(f, id, PL)];
+    }
   }
 }
 
@@ -1238,6 +1230,7 @@ struct PDConfig {
   size_t smem;
   bool persistent = false;
   size_t smem_cq = 0;  // k_pd_tile with the CTA-wide queue (PDArgs::cq)
+  bool tile = false;    // k_pd_tile: half-step schedule (PDArgs::nhalf)
 };
 
 template <int TW, int BY, int PY>
@@ -1257,6 +1250,7 @@ PDConfig make_cfg(int idx) {
   using G = PDGeom<TW, BY, PY>;
   PDConfig c{idx, TW, G::TH, BY, &k_pd_tile<TW, BY, PY, MINB>, G::smem};
   c.smem_cq = 6 * G::PLANE * sizeof(double) + (2 * G::NP * 32 * BY + 2) * sizeof(int);
+  c.tile = true;
   return c;
 }
 
@@ -1306,7 +1300,7 @@ int pd_launch(const PDConfig &c, const PDArgs &a, int nb, cudaStream_t s) {
   }
   // the CTA-wide projection queue needs 4 B per pair instead of the per-warp
   // 16 B: smaller carve-out, larger L1
-  const size_t smem = a.cq && c.smem_cq ? c.smem_cq : c.smem;
+  const size_t smem = c.tile ? c.smem_cq : c.smem;
   c.fn<<<grid, dim3(32, c.by), smem, s>>>(a);
   count_launch();
   return FT_OK;
@@ -1411,6 +1405,49 @@ int launch_level_cluster(const LevelArgs &a, int nb, cudaStream_t s) {
 // Time the dominant kernel alone: `reps` eager launches of the finest-level
 // primal-dual tile kernel over the workspace's current state (as left by the
 // last step), bracketed by CUDA events on `s`.  Returns the mean duration.
+// Half-step schedule of one k_pd_tile launch (PDArgs::nhalf / first / last)
+// and its shrinking cone: the rows each half-step must compute, propagated
+// backwards from the written interior [halo, th-halo).  A dual step at row r
+// reads u-bar at r, r+1 and its own p; a primal step reads p at r, r-1.
+// Returns false if the schedule needs rows outside the tile (too many
+// half-steps for the halo).
+bool halfstep_schedule(PDArgs &a, bool first, int nhalf, bool last, int halo, int th) {
+  a.first = first;
+  a.nhalf = nhalf;
+  a.last = last;
+  a.cone_rows = 0;
+  if (halo == 0) return true;  // the tile is the whole level: every row is needed
+  if (nhalf > 16) return false;
+  const int kNone = 1 << 20;
+  int ulo = halo, uhi = th - halo;                             // u needed after step j
+  int plo = last ? kNone : halo, phi = last ? -kNone : th - halo;  // p needed
+  int blo = kNone, bhi = -kNone;                               // u-bar needed
+  for (int j = nhalf - 1; j >= 0; --j) {
+    const bool dual = ((j & 1) == 0) == first;
+    int lo, hi;
+    if (dual) {
+      lo = plo;
+      hi = phi;
+      if (lo < hi) blo = std::min(blo, lo), bhi = std::max(bhi, hi + 1);
+    } else {
+      lo = std::min(ulo, blo);
+      hi = std::max(uhi, bhi);
+      plo = std::min(plo, lo - 1);
+      phi = std::max(phi, hi);
+      ulo = lo, uhi = hi;
+      blo = kNone, bhi = -kNone;
+    }
+    if (lo >= hi) lo = hi = 0;
+    if (lo < 0 || hi > th) return false;
+    a.rows_lo[j] = (signed char)lo;
+    a.rows_hi[j] = (signed char)hi;
+  }
+  if ((plo < phi && (plo < 0 || phi > th)) || ulo < 0 || uhi > th) return false;
+  if (first && blo < bhi && (blo < 0 || bhi > th)) return false;  // u-bar = u on [0, th)
+  a.cone_rows = 1;
+  return true;
+}
+
 int profile_pd(FlowWork &fw, int w, int h, int nb, const FlowParamsD &p, int reps,
                cudaStream_t s, double *ms_per_launch, int *iters_per_launch) {
   const PDPlan plan = pd_plan(w, h);
@@ -1433,6 +1470,11 @@ int profile_pd(FlowWork &fw, int w, int h, int nb, const FlowParamsD &p, int rep
   a.cone = env_int("FT_PD_CONE", 1);
   a.cq = env_int("FT_PD_CQ", 1);
   a.async_ld = env_int("FT_PD_ASYNC", 1);
+  if (plan.cfg.tile) {  // a middle launch: `iters` primal + dual pairs
+    if (!halfstep_schedule(a, false, 2 * iters, false, halo, plan.cfg.th))
+      return fail(FT_EINVAL, "FT_PD_PROFILE_ITERS exceeds the halo");
+    if (!a.cone) a.cone_rows = 0;
+  }
   a.tau = p.tau;
   a.lam = p.lam;
   a.sigma = 1.0 / (8.0 * p.tau);
@@ -1588,9 +1630,18 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
         const int si = span && span->spans < PdSpan::kMaxSpans ? span->spans : -1;
         if (si >= 0)
           FT_CUDA_TRY(cudaEventRecordWithFlags(span->ev[2 * si], s, cudaEventRecordExternal));
+        // k_pd_tile: 2*iters half-steps D P D P ... split into launches that
+        // end after a dual step (state u, p) -- the first of at most 2*halo-1
+        // half-steps (starts with D), then 2*halo (P..D), and the rest (odd,
+        // P..P) in the last launch.  Other kernels: `halo` whole iterations.
+        const int total = plan.cfg.tile ? 2 * p.iters : p.iters;
         int done = 0;
-        while (done < p.iters) {
-          const int n = resident ? p.iters : std::min(halo, p.iters - done);
+        while (done < total) {
+          int n;
+          if (!plan.cfg.tile) n = resident ? p.iters : std::min(halo, p.iters - done);
+          else if (resident) n = total;
+          else if (done == 0) n = std::min(2 * halo - 1, total);
+          else n = total - done <= 2 * halo ? total - done : 2 * halo;
           PDArgs a;
           a.in = sp(cur);
           a.out = sp(1 - cur);
@@ -1608,6 +1659,11 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
           a.cone = env_int("FT_PD_CONE", 1);
           a.cq = env_int("FT_PD_CQ", 1);
           a.async_ld = env_int("FT_PD_ASYNC", 1);
+          if (plan.cfg.tile) {
+            if (!halfstep_schedule(a, done == 0, n, done + n == total, halo, plan.cfg.th))
+              return fail(FT_EINVAL, "primal-dual schedule exceeds the tile halo");
+            if (!a.cone) a.cone_rows = 0;
+          }
           a.tau = p.tau;
           a.lam = p.lam;
           a.sigma = sigma;

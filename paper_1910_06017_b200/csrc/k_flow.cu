@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <type_traits>
 
 #include <cooperative_groups.h>
 
@@ -716,6 +717,8 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const PDArgs a) {
   }
 }
 
+#include "pd_sweep.cuh"
+
 // ------------------------------------------------------------------------
 // Register-strip variant.  Tile = 32 columns x (BY*PY) rows; lane = column,
 // warp w owns rows [w*PY, w*PY+PY) as a vertical strip held entirely in
@@ -1306,16 +1309,77 @@ int pd_launch(const PDConfig &c, const PDArgs &a, int nb, cudaStream_t s) {
   return FT_OK;
 }
 
+int env_int(const char *name, int dflt) {
+  const char *v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+
+// k_pd_sweep launches: `nh` half-steps, starting with a dual step when
+// `first` (the warp's first launch).  pow2 time steps only (the default);
+// other tau use k_pd_tile.
+constexpr int kSweepSlots = 4;  // input ring rows (prefetch distance 1 row)
+constexpr int kSweepMinB = 8;   // resident warps per SM
+
+using SweepFn = void (*)(SweepArgs);
+
+int sweep_launch(const PDArgs &pa, int nh, bool first, int nb, cudaStream_t s) {
+  SweepFn fn = nullptr;
+  size_t smem = 0;
+#define FT_SWEEP_CASE(NH_, FD_)                                                \
+  case (FD_ ? 0 : 16) + NH_:                                                   \
+    fn = &k_pd_sweep<NH_, FD_, true, kSweepSlots, (NH_ <= 4 ? 16 : kSweepMinB)>; \
+    smem = SweepGeom<NH_, kSweepSlots>::smem_per_warp;                         \
+    break;
+  switch ((first ? 0 : 16) + nh) {
+    FT_SWEEP_CASE(2, true)
+    FT_SWEEP_CASE(3, true)
+    FT_SWEEP_CASE(4, true)
+    FT_SWEEP_CASE(6, true)
+    FT_SWEEP_CASE(7, true)
+    FT_SWEEP_CASE(1, false)
+    FT_SWEEP_CASE(3, false)
+    FT_SWEEP_CASE(4, false)
+    FT_SWEEP_CASE(5, false)
+    FT_SWEEP_CASE(7, false)
+    FT_SWEEP_CASE(8, false)
+    default: return fail(FT_EINVAL, "k_pd_sweep: unsupported half-step count");
+  }
+#undef FT_SWEEP_CASE
+  static SweepFn attr_done[32] = {};
+  const int key = (first ? 0 : 16) + nh;
+  if (attr_done[key] != fn) {
+    FT_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    attr_done[key] = fn;
+  }
+  SweepArgs a;
+  a.in = pa.in;
+  a.out = pa.out;
+  a.gx = pa.gx;
+  a.gy = pa.gy;
+  a.r0 = pa.r0;
+  a.w = pa.w;
+  a.h = pa.h;
+  a.cap = pa.cap;
+  a.seg = std::max(1, env_int("FT_SWEEP_SEG", 64));
+  const int strip = 32 - 2 * ((nh + 1) / 2);  // interior columns per warp
+  a.nstrips = (pa.w + strip - 1) / strip;
+  sweep_cone(first, nh, a.cA, a.cB);
+  a.tau = pa.tau;
+  a.tl = pa.tau * pa.lam;
+  a.sigma = pa.sigma;
+  a.shrink = pa.shrink;
+  const dim3 grid(a.nstrips, (pa.h + a.seg - 1) / a.seg, nb);
+  fn<<<grid, dim3(32, 1), smem, s>>>(a);
+  count_launch();
+  return FT_OK;
+}
+
 // tile configuration + halo used for a level of w x h
 struct PDPlan {
   PDConfig cfg;
   int halo;
 };
 
-int env_int(const char *name, int dflt) {
-  const char *v = getenv(name);
-  return v && *v ? atoi(v) : dflt;
-}
 
 PDPlan pd_plan(int w, int h) {
   // coarse levels that fit one tile run resident (no halo, all iterations)
@@ -1332,6 +1396,10 @@ PDPlan pd_plan(int w, int h) {
 inline int pow2_params(double tau) {
   int e = 0;
   return tau > 0.0 && std::frexp(tau, &e) == 0.5 ? 1 : 0;
+}
+
+bool use_sweep(const PDPlan &plan, double tau) {
+  return plan.cfg.tile && plan.halo == 4 && pow2_params(tau) && env_int("FT_PD_SWEEP", 0) != 0;
 }
 
 inline dim3 grid2d(int w, int h, int nb) { return dim3((w + 31) / 32, (h + 7) / 8, nb); }
@@ -1454,7 +1522,9 @@ int profile_pd(FlowWork &fw, int w, int h, int nb, const FlowParamsD &p, int rep
   const int halo = plan.halo;
   // FT_PD_PROFILE_ITERS overrides the iterations per launch (cost model:
   // load/store overhead vs per-iteration cost)
-  const int iters = env_int("FT_PD_PROFILE_ITERS", halo ? std::min(halo, p.iters) : p.iters);
+  const int hs = use_sweep(plan, p.tau) ? std::max(1, std::min(4, env_int("FT_SWEEP_ITERS", halo)))
+                                        : halo;
+  const int iters = env_int("FT_PD_PROFILE_ITERS", hs ? std::min(hs, p.iters) : p.iters);
   PDArgs a;
   a.gx = fw.gx;
   a.gy = fw.gy;
@@ -1488,7 +1558,8 @@ int profile_pd(FlowWork &fw, int w, int h, int nb, const FlowParamsD &p, int rep
     if (r == 0) FT_CUDA_TRY(cudaEventRecord(e0, s));
     a.in = state_ptrs(fw.st[cur], fw.nb, fw.cap);
     a.out = state_ptrs(fw.st[1 - cur], fw.nb, fw.cap);
-    FT_TRY(pd_launch(plan.cfg, a, nb, s));
+    if (use_sweep(plan, p.tau)) FT_TRY(sweep_launch(a, 2 * iters, false, nb, s));
+    else FT_TRY(pd_launch(plan.cfg, a, nb, s));
     cur = 1 - cur;
   }
   FT_CUDA_TRY(cudaEventRecord(e1, s));
@@ -1603,6 +1674,11 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
     const PDPlan plan = pd_plan(w, h);
     const bool resident = plan.halo == 0;
     const int halo = plan.halo;
+    // barrier-free row sweep (k_pd_sweep) for tiled levels: same launch
+    // schedule (<= 8 half-steps per launch), power-of-two time steps
+    const bool sweep = use_sweep(plan, p.tau);
+    // iterations per launch: the tile halo, or FT_SWEEP_ITERS (<= 4) for the sweep
+    const int hs = sweep ? std::max(1, std::min(4, env_int("FT_SWEEP_ITERS", halo))) : halo;
     // Stream groups (FT_PD_GROUP, finest level): a group of streams runs all
     // of its warps before the next group starts, so the group's state planes
     // (~63 MB per SD stream incl. ping-pong) can stay resident in the 126 MB
@@ -1640,8 +1716,8 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
           int n;
           if (!plan.cfg.tile) n = resident ? p.iters : std::min(halo, p.iters - done);
           else if (resident) n = total;
-          else if (done == 0) n = std::min(2 * halo - 1, total);
-          else n = total - done <= 2 * halo ? total - done : 2 * halo;
+          else if (done == 0) n = std::min(2 * hs - 1, total);
+          else n = total - done <= 2 * hs ? total - done : 2 * hs;
           PDArgs a;
           a.in = sp(cur);
           a.out = sp(1 - cur);
@@ -1668,7 +1744,8 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
           a.lam = p.lam;
           a.sigma = sigma;
           a.shrink = shrink;
-          FT_TRY(pd_launch(plan.cfg, a, gn, s));
+          if (sweep) FT_TRY(sweep_launch(a, n, done == 0, gn, s));
+          else FT_TRY(pd_launch(plan.cfg, a, gn, s));
           cur = 1 - cur;
           done += n;
           if (si >= 0) ++span->launches;

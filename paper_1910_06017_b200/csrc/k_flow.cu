@@ -1325,11 +1325,18 @@ using SweepFn = void (*)(SweepArgs);
 int sweep_launch(const PDArgs &pa, int nh, bool first, int nb, cudaStream_t s) {
   SweepFn fn = nullptr;
   size_t smem = 0;
-#define FT_SWEEP_CASE(NH_, FD_)                                                \
-  case (FD_ ? 0 : 16) + NH_:                                                   \
-    fn = &k_pd_sweep<NH_, FD_, true, kSweepSlots, (NH_ <= 4 ? 16 : kSweepMinB)>; \
-    smem = SweepGeom<NH_, kSweepSlots>::smem_per_warp;                         \
+#define FT_SWEEP_CASE(NH_, FD_)                                                  \
+  case (FD_ ? 0 : 16) + NH_:                                                     \
+    if (cols == 2 && NH_ <= 4) {                                                 \
+      fn = &k_pd_sweep<NH_, FD_, true, kSweepSlots, 6, (NH_ <= 4 ? 2 : 1)>;     \
+      smem = SweepGeom<NH_, kSweepSlots, (NH_ <= 4 ? 2 : 1)>::smem_per_warp;    \
+    } else {                                                                     \
+      fn = &k_pd_sweep<NH_, FD_, true, kSweepSlots, (NH_ <= 4 ? 16 : kSweepMinB), 1>; \
+      smem = SweepGeom<NH_, kSweepSlots, 1>::smem_per_warp;                      \
+      cols = 1;                                                                  \
+    }                                                                            \
     break;
+  int cols = env_int("FT_SWEEP_COLS", 2);
   switch ((first ? 0 : 16) + nh) {
     FT_SWEEP_CASE(2, true)
     FT_SWEEP_CASE(3, true)
@@ -1345,8 +1352,8 @@ int sweep_launch(const PDArgs &pa, int nh, bool first, int nb, cudaStream_t s) {
     default: return fail(FT_EINVAL, "k_pd_sweep: unsupported half-step count");
   }
 #undef FT_SWEEP_CASE
-  static SweepFn attr_done[32] = {};
-  const int key = (first ? 0 : 16) + nh;
+  static SweepFn attr_done[64] = {};
+  const int key = (first ? 0 : 16) + nh + (cols == 2 ? 32 : 0);
   if (attr_done[key] != fn) {
     FT_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     attr_done[key] = fn;
@@ -1361,7 +1368,8 @@ int sweep_launch(const PDArgs &pa, int nh, bool first, int nb, cudaStream_t s) {
   a.h = pa.h;
   a.cap = pa.cap;
   a.seg = std::max(1, env_int("FT_SWEEP_SEG", 64));
-  const int strip = 32 - 2 * ((nh + 1) / 2);  // interior columns per warp
+  const int khalo = cols == 1 ? (nh + 1) / 2 : ((nh + 1) / 2 + 1) / 2 * 2;
+  const int strip = 32 * cols - 2 * khalo;  // interior columns per warp
   a.nstrips = (pa.w + strip - 1) / strip;
   sweep_cone(first, nh, a.cA, a.cB);
   a.tau = pa.tau;
@@ -1522,7 +1530,7 @@ int profile_pd(FlowWork &fw, int w, int h, int nb, const FlowParamsD &p, int rep
   const int halo = plan.halo;
   // FT_PD_PROFILE_ITERS overrides the iterations per launch (cost model:
   // load/store overhead vs per-iteration cost)
-  const int hs = use_sweep(plan, p.tau) ? std::max(1, std::min(4, env_int("FT_SWEEP_ITERS", halo)))
+  const int hs = use_sweep(plan, p.tau) ? std::max(1, std::min(4, env_int("FT_SWEEP_ITERS", 2)))
                                         : halo;
   const int iters = env_int("FT_PD_PROFILE_ITERS", hs ? std::min(hs, p.iters) : p.iters);
   PDArgs a;
@@ -1678,7 +1686,7 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
     // schedule (<= 8 half-steps per launch), power-of-two time steps
     const bool sweep = use_sweep(plan, p.tau);
     // iterations per launch: the tile halo, or FT_SWEEP_ITERS (<= 4) for the sweep
-    const int hs = sweep ? std::max(1, std::min(4, env_int("FT_SWEEP_ITERS", halo))) : halo;
+    const int hs = sweep ? std::max(1, std::min(4, env_int("FT_SWEEP_ITERS", 2))) : halo;
     // Stream groups (FT_PD_GROUP, finest level): a group of streams runs all
     // of its warps before the next group starts, so the group's state planes
     // (~63 MB per SD stream incl. ping-pong) can stay resident in the 126 MB

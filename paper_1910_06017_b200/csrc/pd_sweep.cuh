@@ -41,12 +41,20 @@ struct SweepArgs {
   double tau, tl, sigma, shrink;
 };
 
-template <int NH, int NSLOT>
+// C = columns per lane (1 or 2): a warp covers 32*C columns, of which the
+// outer K on each side are halo.
+template <int NH, int C>
+__host__ __device__ constexpr int sweep_halo() {
+  return C == 1 ? (NH + 1) / 2 : ((NH + 1) / 2 + 1) / 2 * 2;  // even for C = 2 (16-byte pairs)
+}
+
+template <int NH, int NSLOT, int C>
 struct SweepGeom {
-  static constexpr int CR = 8;  // constant-ring rows (>= NH)
-  static constexpr int RING = NSLOT * 9 * 32;   // doubles: u1 u2 p11 p12 p21 p22 gx gy r0
-  static constexpr int CRING = CR * 5 * 32;     // doubles: gx gy r0 thr ig2
-  static constexpr int QUEUE = (NH + 1) / 2 * 2 * 32 * 2;  // doubles: 2 pairs per dual stage per lane
+  static constexpr int NC = 32 * C;               // columns per warp
+  static constexpr int CR = NH <= 4 ? 4 : 8;      // constant-ring rows (>= NH)
+  static constexpr int RING = NSLOT * 9 * NC;     // doubles: u1 u2 p11 p12 p21 p22 gx gy r0
+  static constexpr int CRING = CR * 5 * NC;       // doubles: gx gy r0 thr ig2
+  static constexpr int QUEUE = (NH + 1) / 2 * 2 * NC * 2;  // doubles: 2 pairs per dual stage per column
   static constexpr int PER_WARP = RING + CRING + QUEUE;
   static constexpr size_t smem_per_warp = PER_WARP * sizeof(double);
   static_assert(NH <= CR, "constant ring too short for the stage lags");
@@ -58,12 +66,20 @@ __host__ __device__ constexpr bool sweep_is_dual(int j) {
   return ((j & 1) == 0) == FIRSTD;
 }
 
-template <int NH, bool FIRSTD, bool P2, int NSLOT, int MINB>
+__device__ __forceinline__ void cp_async16(double *dst, const double *src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const int n = valid ? 16 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(n));
+}
+
+template <int NH, bool FIRSTD, bool P2, int NSLOT, int MINB, int C>
 __global__ void __launch_bounds__(32, MINB) k_pd_sweep(const SweepArgs a) {
-  using G = SweepGeom<NH, NSLOT>;
-  constexpr int K = (NH + 1) / 2;  // strip halo: the launch's x dependency cone
+  using G = SweepGeom<NH, NSLOT, C>;
+  constexpr int NC = G::NC;
+  constexpr int K = sweep_halo<NH, C>();  // strip halo: the launch's x dependency cone
   static_assert(NH >= 1 && NH <= 8, "at most 8 half-steps per launch");
-  constexpr int STRIP = 32 - 2 * K;
+  static_assert(C == 1 || C == 2, "one or two columns per lane");
+  constexpr int STRIP = NC - 2 * K;
   constexpr int PF = NSLOT - 3;  // rows prefetched beyond s+1
   constexpr int L = NH - 1;      // last stage
   constexpr bool END_D = sweep_is_dual<FIRSTD>(L);
@@ -77,10 +93,19 @@ __global__ void __launch_bounds__(32, MINB) k_pd_sweep(const SweepArgs a) {
   double2 *const queue = reinterpret_cast<double2 *>(sm + G::RING + G::CRING);
 
   const int W = a.w, H = a.h;
-  const int x = strip * STRIP - K + lane;
-  const bool xin = x >= 0 && x < W;
-  const bool wr = xin && lane >= K && lane < 32 - K;
-  const bool fR = x < W - 1, fL = x > 0, fLC = x == W - 1;
+  const int x0 = strip * STRIP - K + C * lane;  // this lane's first column
+  // 16-byte global pairs: even width and plane capacity (x0 is even for C=2)
+  const bool vec = C == 2 && (W & 1) == 0 && (a.cap & 1) == 0;
+  bool xin[C], wr[C], fR[C], fL[C], fLC[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    const int x = x0 + c;
+    xin[c] = x >= 0 && x < W;
+    wr[c] = xin[c] && C * lane + c >= K && C * lane + c < NC - K;
+    fR[c] = x < W - 1;
+    fL[c] = x > 0;
+    fLC[c] = x == W - 1;
+  }
   const int y0 = blockIdx.y * a.seg, y1 = min(y0 + a.seg, H);
   const int64_t so = (int64_t)blockIdx.z * a.cap;
   const unsigned lt_mask = (1u << lane) - 1u;
@@ -97,21 +122,45 @@ __global__ void __launch_bounds__(32, MINB) k_pd_sweep(const SweepArgs a) {
   const int s0 = lo[0];
   const int lr0 = max(lo[0] - 1, 0), lr1 = min(hi[0] + 1, H);  // input rows to load
 
-  // ---- input ring: row r -> slot r & (NSLOT-1), 9 planes x 32 lanes
+  // ---- input ring: row r -> slot r & (NSLOT-1), 9 planes x NC columns
   auto load_row = [&](int r) {
     if (r < lr0 || r >= lr1) return;
-    double *dst = ring + (r & (NSLOT - 1)) * 9 * 32 + lane;
-    const int64_t o = so + (int64_t)r * W + x;
+    double *dst = ring + (r & (NSLOT - 1)) * 9 * NC + C * lane;
+    const int64_t o = so + (int64_t)r * W + x0;
     const double *src[9] = {a.in.p[U1], a.in.p[U2], a.in.p[P11], a.in.p[P12], a.in.p[P21],
                             a.in.p[P22], a.gx, a.gy, a.r0};
 #pragma unroll
     for (int f = 0; f < 9; ++f) {
       if (FIRSTD && f >= 2 && f < 6) continue;  // p = 0 at the start of a warp
-      cp_async8(dst + f * 32, xin ? src[f] + o : src[f], xin);
+      if (C == 2 && vec) {
+        cp_async16(dst + f * NC, xin[0] ? src[f] + o : src[f], xin[0]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < C; ++c) cp_async8(dst + f * NC + c, xin[c] ? src[f] + o + c : src[f], xin[c]);
+      }
     }
   };
-  auto rd = [&](int r, int f) -> double { return ring[(r & (NSLOT - 1)) * 9 * 32 + f * 32 + lane]; };
-  auto crd = [&](int r, int f) -> double { return cring[(r & (G::CR - 1)) * 5 * 32 + f * 32 + lane]; };
+  // this lane's C values of plane f in ring row r / constant row r
+  auto rd = [&](int r, int f, double *v) {
+    const double *q = ring + (r & (NSLOT - 1)) * 9 * NC + f * NC + C * lane;
+    if (C == 2) {
+      const double2 t = *reinterpret_cast<const double2 *>(q);
+      v[0] = t.x;
+      v[C - 1] = t.y;
+    } else {
+      v[0] = q[0];
+    }
+  };
+  auto crd = [&](int r, int f, double *v) {
+    const double *q = cring + (r & (G::CR - 1)) * 5 * NC + f * NC + C * lane;
+    if (C == 2) {
+      const double2 t = *reinterpret_cast<const double2 *>(q);
+      v[0] = t.x;
+      v[C - 1] = t.y;
+    } else {
+      v[0] = q[0];
+    }
+  };
 
   // prologue: rows s0-1 .. s0+1 as one group, then s0+2 .. s0+PF one group each
   load_row(s0 - 1);
@@ -129,27 +178,35 @@ __global__ void __launch_bounds__(32, MINB) k_pd_sweep(const SweepArgs a) {
   // age 1 (previous step) and slot PA age 2; the step's outputs replace slot
   // PA.  Alternating the slot names (two step bodies per loop iteration)
   // keeps the carries in place -- no register moves.
-  double pX[NH][2][4], uX[NH][2][2], bX[NH][2][2];
+  double pX[NH][2][4][C], uX[NH][2][2][C], bX[NH][2][2][C];
 #pragma unroll
   for (int j = 0; j < NH; ++j)
 #pragma unroll
-    for (int t = 0; t < 2; ++t) {
+    for (int t = 0; t < 2; ++t)
 #pragma unroll
-      for (int c = 0; c < 4; ++c) pX[j][t][c] = 0.0;
+      for (int c = 0; c < C; ++c) {
 #pragma unroll
-      for (int c = 0; c < 2; ++c) uX[j][t][c] = bX[j][t][c] = 0.0;
-    }
+        for (int k = 0; k < 4; ++k) pX[j][t][k][c] = 0.0;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) uX[j][t][k][c] = bX[j][t][k][c] = 0.0;
+      }
 
   auto const_row = [&](int r) {
-    const double vgx = rd(r, 6), vgy = rd(r, 7), vr0 = rd(r, 8);
-    const double g2 = vgx * vgx + vgy * vgy;
-    const bool ok = g2 > 1e-12;
-    double *c = cring + (r & (G::CR - 1)) * 5 * 32 + lane;
-    c[0 * 32] = vgx;
-    c[1 * 32] = vgy;
-    c[2 * 32] = vr0;
-    c[3 * 32] = tl * g2;
-    c[4 * 32] = ok ? 1.0 / (g2 > 1e-12 ? g2 : 1e-12) : 0.0;
+    double vgx[C], vgy[C], vr0[C];
+    rd(r, 6, vgx);
+    rd(r, 7, vgy);
+    rd(r, 8, vr0);
+    double *q = cring + (r & (G::CR - 1)) * 5 * NC + C * lane;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const double g2 = vgx[c] * vgx[c] + vgy[c] * vgy[c];
+      const bool ok = g2 > 1e-12;
+      q[0 * NC + c] = vgx[c];
+      q[1 * NC + c] = vgy[c];
+      q[2 * NC + c] = vr0[c];
+      q[3 * NC + c] = tl * g2;
+      q[4 * NC + c] = ok ? 1.0 / (g2 > 1e-12 ? g2 : 1e-12) : 0.0;
+    }
   };
 
   int s = s0;
@@ -163,50 +220,65 @@ __global__ void __launch_bounds__(32, MINB) k_pd_sweep(const SweepArgs a) {
     cp_async_commit();
     asm volatile("cp.async.wait_group %0;\n" ::"n"(PF) : "memory");
     if (s == s0 && s0 < lr1) const_row(s0);
-    // constants of row s+1 (optflow.py:163-176), read by the primal stages
-    // from the next step on (the division stays off this step's chain)
-    if (s + 1 < lr1) const_row(s + 1);
 
-    double pF[NH][4], uF[NH][2], bF[NH][2];
+    double pF[NH][4][C], uF[NH][2][C], bF[NH][2][C];
     // ---- primal stages (:194-208): rows s - j
 #pragma unroll
     for (int j = 0; j < NH; ++j) {
       if (sweep_is_dual<FIRSTD>(j)) continue;
       const int r = s - j;
-      double p11, p12, p21, p22, q12, q22, u1, u2;
+      double p11[C], p12[C], p21[C], p22[C], q12[C], q22[C], u1[C], u2[C];
       if (j == 0) {  // input p at rows r, r-1 and u at r
-        p11 = rd(r, 2); p12 = rd(r, 3); p21 = rd(r, 4); p22 = rd(r, 5);
-        q12 = rd(r - 1, 3); q22 = rd(r - 1, 5);
-        u1 = rd(r, 0); u2 = rd(r, 1);
+        rd(r, 2, p11); rd(r, 3, p12); rd(r, 4, p21); rd(r, 5, p22);
+        rd(r - 1, 3, q12); rd(r - 1, 5, q22);
+        rd(r, 0, u1); rd(r, 1, u2);
       } else {
-        p11 = pX[j - 1][PB][0]; p12 = pX[j - 1][PB][1]; p21 = pX[j - 1][PB][2]; p22 = pX[j - 1][PB][3];
-        q12 = pX[j - 1][PA][1]; q22 = pX[j - 1][PA][3];
-        if (j == 1) { u1 = rd(r, 0); u2 = rd(r, 1); }
-        else { u1 = uX[j - 2][PA][0]; u2 = uX[j - 2][PA][1]; }
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          p11[c] = pX[j - 1][PB][0][c]; p12[c] = pX[j - 1][PB][1][c];
+          p21[c] = pX[j - 1][PB][2][c]; p22[c] = pX[j - 1][PB][3][c];
+          q12[c] = pX[j - 1][PA][1][c]; q22[c] = pX[j - 1][PA][3][c];
+        }
+        if (j == 1) { rd(r, 0, u1); rd(r, 1, u2); }
+        else {
+#pragma unroll
+          for (int c = 0; c < C; ++c) u1[c] = uX[j - 2][PA][0][c], u2[c] = uX[j - 2][PA][1][c];
+        }
       }
-      const double l11 = __shfl_up_sync(0xffffffffu, p11, 1);
-      const double l21 = __shfl_up_sync(0xffffffffu, p21, 1);
+      // p at x-1: the lane's previous column, or lane-1's last one
+      double l11[C], l21[C];
+      l11[0] = __shfl_up_sync(0xffffffffu, p11[C - 1], 1);
+      l21[0] = __shfl_up_sync(0xffffffffu, p21[C - 1], 1);
+#pragma unroll
+      for (int c = 1; c < C; ++c) l11[c] = p11[c - 1], l21[c] = p21[c - 1];
+      double gx[C], gy[C], r0[C], thr[C], ig2[C];
+      crd(r, 0, gx); crd(r, 1, gy); crd(r, 2, r0); crd(r, 3, thr); crd(r, 4, ig2);
       const bool U = r > 0, LR = r == H - 1;
-      // divergence (imageops.py:41-50) with the reference's border rules
-      const double dx1 = fL ? (fLC ? -l11 : p11 - l11) : p11;
-      const double dx2 = fL ? (fLC ? -l21 : p21 - l21) : p21;
-      const double dy1 = U ? (LR ? -q12 : p12 - q12) : p12;
-      const double dy2 = U ? (LR ? -q22 : p22 - q22) : p22;
-      const double v1 = madx<P2>(tau, dx1 + dy1, u1);
-      const double v2 = madx<P2>(tau, dx2 + dy2, u2);
-      const double gx = crd(r, 0), gy = crd(r, 1), r0 = crd(r, 2), thr = crd(r, 3), ig2 = crd(r, 4);
-      const double rho = r0 + gx * v1 + gy * v2;
-      const bool lo_ = rho < -thr;
-      const bool hi_ = rho > thr;
-      double d = lo_ ? tl : (hi_ ? -tl : -rho * ig2);
-      d = (ig2 != 0.0 || lo_ || hi_) ? d : 0.0;  // ig2 != 0 <=> |grad|^2 > 1e-12
-      const double n1 = v1 + d * gx;
-      const double n2 = v2 + d * gy;
-      uF[j][0] = n1;
-      uF[j][1] = n2;
-      bF[j][0] = madx<true>(2.0, n1, -u1);
-      bF[j][1] = madx<true>(2.0, n2, -u2);
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        // divergence (imageops.py:41-50) with the reference's border rules
+        const double dx1 = fL[c] ? (fLC[c] ? -l11[c] : p11[c] - l11[c]) : p11[c];
+        const double dx2 = fL[c] ? (fLC[c] ? -l21[c] : p21[c] - l21[c]) : p21[c];
+        const double dy1 = U ? (LR ? -q12[c] : p12[c] - q12[c]) : p12[c];
+        const double dy2 = U ? (LR ? -q22[c] : p22[c] - q22[c]) : p22[c];
+        const double v1 = madx<P2>(tau, dx1 + dy1, u1[c]);
+        const double v2 = madx<P2>(tau, dx2 + dy2, u2[c]);
+        const double rho = r0[c] + gx[c] * v1 + gy[c] * v2;
+        const bool lo_ = rho < -thr[c];
+        const bool hi_ = rho > thr[c];
+        double d = lo_ ? tl : (hi_ ? -tl : -rho * ig2[c]);
+        d = (ig2[c] != 0.0 || lo_ || hi_) ? d : 0.0;  // ig2 != 0 <=> |grad|^2 > 1e-12
+        const double n1 = v1 + d * gx[c];
+        const double n2 = v2 + d * gy[c];
+        uF[j][0][c] = n1;
+        uF[j][1][c] = n2;
+        bF[j][0][c] = madx<true>(2.0, n1, -u1[c]);
+        bF[j][1][c] = madx<true>(2.0, n2, -u2[c]);
+      }
     }
+    // constants of row s+1 (optflow.py:163-176) for the next step's primal
+    // stages (after this step's reads: the slot it replaces held row s+1-CR)
+    if (s + 1 < lr1) const_row(s + 1);
 
     // ---- dual stages (:180-185), unprojected: rows s - j
     unsigned need = 0;
@@ -214,53 +286,72 @@ __global__ void __launch_bounds__(32, MINB) k_pd_sweep(const SweepArgs a) {
     for (int j = 0; j < NH; ++j) {
       if (!sweep_is_dual<FIRSTD>(j)) continue;
       const int r = s - j;
-      double c1, c2, d1, d2, o11, o12, o21, o22;
+      double c1[C], c2[C], d1[C], d2[C], o11[C], o12[C], o21[C], o22[C];
       if (j == 0) {  // first launch: u-bar = u, p = 0
-        c1 = rd(r, 0); c2 = rd(r, 1); d1 = rd(r + 1, 0); d2 = rd(r + 1, 1);
-        o11 = o12 = o21 = o22 = 0.0;
+        rd(r, 0, c1); rd(r, 1, c2); rd(r + 1, 0, d1); rd(r + 1, 1, d2);
+#pragma unroll
+        for (int c = 0; c < C; ++c) o11[c] = o12[c] = o21[c] = o22[c] = 0.0;
       } else {
-        c1 = bX[j - 1][PB][0]; c2 = bX[j - 1][PB][1]; d1 = bF[j - 1][0]; d2 = bF[j - 1][1];
-        if (j == 1) { o11 = rd(r, 2); o12 = rd(r, 3); o21 = rd(r, 4); o22 = rd(r, 5); }
-        else { o11 = pX[j - 2][PA][0]; o12 = pX[j - 2][PA][1]; o21 = pX[j - 2][PA][2]; o22 = pX[j - 2][PA][3]; }
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          c1[c] = bX[j - 1][PB][0][c]; c2[c] = bX[j - 1][PB][1][c];
+          d1[c] = bF[j - 1][0][c]; d2[c] = bF[j - 1][1][c];
+        }
+        if (j == 1) { rd(r, 2, o11); rd(r, 3, o12); rd(r, 4, o21); rd(r, 5, o22); }
+        else {
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            o11[c] = pX[j - 2][PA][0][c]; o12[c] = pX[j - 2][PA][1][c];
+            o21[c] = pX[j - 2][PA][2][c]; o22[c] = pX[j - 2][PA][3][c];
+          }
+        }
       }
-      const double r1 = __shfl_down_sync(0xffffffffu, c1, 1);
-      const double r2 = __shfl_down_sync(0xffffffffu, c2, 1);
+      // u-bar at x+1: the lane's next column, or lane+1's first one
+      double r1[C], r2[C];
+      r1[C - 1] = __shfl_down_sync(0xffffffffu, c1[0], 1);
+      r2[C - 1] = __shfl_down_sync(0xffffffffu, c2[0], 1);
+#pragma unroll
+      for (int c = 0; c + 1 < C; ++c) r1[c] = c1[c + 1], r2[c] = c2[c + 1];
       const bool D = r < H - 1;
-      const double a1x = fR ? r1 - c1 : 0.0;
-      const double a1y = D ? d1 - c1 : 0.0;
-      const double a2x = fR ? r2 - c2 : 0.0;
-      const double a2y = D ? d2 - c2 : 0.0;
-      const double p11 = madx<P2>(sigma, a1x, o11) * shrink;
-      const double p12 = madx<P2>(sigma, a1y, o12) * shrink;
-      const double p21 = madx<P2>(sigma, a2x, o21) * shrink;
-      const double p22 = madx<P2>(sigma, a2y, o22) * shrink;
-      pF[j][0] = p11; pF[j][1] = p12; pF[j][2] = p21; pF[j][3] = p22;
-      // screening test only (not reference arithmetic): fused is fine.
-      // Rows outside the stage's cone are never read: no projection.
       const unsigned valid = (r >= lo[j] && r < hi[j]) ? 3u : 0u;
-      const unsigned sat = (fma(p11, p11, p12 * p12) > 0.999999 ? 1u : 0u) |
-                           (fma(p21, p21, p22 * p22) > 0.999999 ? 2u : 0u);
-      need |= (sat & valid) << (2 * j);
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const double a1x = fR[c] ? r1[c] - c1[c] : 0.0;
+        const double a1y = D ? d1[c] - c1[c] : 0.0;
+        const double a2x = fR[c] ? r2[c] - c2[c] : 0.0;
+        const double a2y = D ? d2[c] - c2[c] : 0.0;
+        const double p11 = madx<P2>(sigma, a1x, o11[c]) * shrink;
+        const double p12 = madx<P2>(sigma, a1y, o12[c]) * shrink;
+        const double p21 = madx<P2>(sigma, a2x, o21[c]) * shrink;
+        const double p22 = madx<P2>(sigma, a2y, o22[c]) * shrink;
+        pF[j][0][c] = p11; pF[j][1][c] = p12; pF[j][2][c] = p21; pF[j][3][c] = p22;
+        // screening test only (not reference arithmetic): fused is fine.
+        // Rows outside the stage's cone are never read: no projection.
+        const unsigned sat = (fma(p11, p11, p12 * p12) > 0.999999 ? 1u : 0u) |
+                             (fma(p21, p21, p22 * p22) > 0.999999 ? 2u : 0u);
+        need |= (sat & valid) << (2 * (j * C + c));
+      }
     }
 
     // ---- unit-ball projection n = max(1, hypot(.)); p /= n (:186-191),
-    // batched over the dual stages of this step through a per-warp queue
+    // batched over the dual stages of this step through a per-warp queue.
+    // need bit 2*(j*C + c) + k: pair k (0: p11,p12; 1: p21,p22) of column c.
     if (__any_sync(0xffffffffu, need != 0u)) {
-      int off[2 * NH];
+      int off[2 * NH * C];
       int total = 0;
 #pragma unroll
-      for (int k = 0; k < 2 * NH; ++k) {
-        if (!sweep_is_dual<FIRSTD>(k >> 1)) continue;
+      for (int k = 0; k < 2 * NH * C; ++k) {
+        if (!sweep_is_dual<FIRSTD>(k / (2 * C))) continue;
         const unsigned m = __ballot_sync(0xffffffffu, (need >> k) & 1u);
         off[k] = total + __popc(m & lt_mask);
         total += __popc(m);
       }
 #pragma unroll
-      for (int k = 0; k < 2 * NH; ++k) {
-        if (!sweep_is_dual<FIRSTD>(k >> 1)) continue;
+      for (int k = 0; k < 2 * NH * C; ++k) {
+        if (!sweep_is_dual<FIRSTD>(k / (2 * C))) continue;
         if ((need >> k) & 1u) {
-          const int j = k >> 1, c = (k & 1) * 2;
-          queue[off[k]] = make_double2(pF[j][c], pF[j][c + 1]);
+          const int j = k / (2 * C), c = (k >> 1) % C, e = (k & 1) * 2;
+          queue[off[k]] = make_double2(pF[j][e][c], pF[j][e + 1][c]);
         }
       }
       __syncwarp();
@@ -271,51 +362,62 @@ __global__ void __launch_bounds__(32, MINB) k_pd_sweep(const SweepArgs a) {
       }
       __syncwarp();
 #pragma unroll
-      for (int k = 0; k < 2 * NH; ++k) {
-        if (!sweep_is_dual<FIRSTD>(k >> 1)) continue;
+      for (int k = 0; k < 2 * NH * C; ++k) {
+        if (!sweep_is_dual<FIRSTD>(k / (2 * C))) continue;
         if ((need >> k) & 1u) {
-          const int j = k >> 1, c = (k & 1) * 2;
+          const int j = k / (2 * C), c = (k >> 1) % C, e = (k & 1) * 2;
           const double2 v = queue[off[k]];
-          pF[j][c] = v.x;
-          pF[j][c + 1] = v.y;
+          pF[j][e][c] = v.x;
+          pF[j][e + 1][c] = v.y;
         }
       }
       __syncwarp();
     }
 
-    // ---- write back the segment's rows of the last stage (interior lanes)
+    // ---- write back the segment's rows of the last stage (interior columns)
     {
       const int r = s - L;
-      if (r >= y0 && r < y1 && wr) {
-        const int64_t o = so + (int64_t)r * W + x;
+      if (r >= y0 && r < y1) {
+        const int64_t o = so + (int64_t)r * W + x0;
+        auto put = [&](int plane, const double *v) {
+          if (C == 2 && vec) {
+            if (wr[0]) *reinterpret_cast<double2 *>(a.out.p[plane] + o) = make_double2(v[0], v[C - 1]);
+          } else {
+#pragma unroll
+            for (int c = 0; c < C; ++c)
+              if (wr[c]) a.out.p[plane][o + c] = v[c];
+          }
+        };
         if (END_D) {
-          a.out.p[U1][o] = uX[L - 1][PB][0];
-          a.out.p[U2][o] = uX[L - 1][PB][1];
-          a.out.p[P11][o] = pF[L][0];
-          a.out.p[P12][o] = pF[L][1];
-          a.out.p[P21][o] = pF[L][2];
-          a.out.p[P22][o] = pF[L][3];
+          put(U1, uX[L - 1][PB][0]);
+          put(U2, uX[L - 1][PB][1]);
+          put(P11, pF[L][0]);
+          put(P12, pF[L][1]);
+          put(P21, pF[L][2]);
+          put(P22, pF[L][3]);
         } else {
-          a.out.p[U1][o] = uF[L][0];
-          a.out.p[U2][o] = uF[L][1];
+          put(U1, uF[L][0]);
+          put(U2, uF[L][1]);
         }
       }
     }
 
     // ---- this step's outputs replace the age-2 slot
 #pragma unroll
-    for (int j = 0; j < NH; ++j) {
-      if (sweep_is_dual<FIRSTD>(j)) {
+    for (int j = 0; j < NH; ++j)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) pX[j][PA][c] = pF[j][c];
-      } else {
+      for (int c = 0; c < C; ++c) {
+        if (sweep_is_dual<FIRSTD>(j)) {
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          uX[j][PA][c] = uF[j][c];
-          bX[j][PA][c] = bF[j][c];
+          for (int k = 0; k < 4; ++k) pX[j][PA][k][c] = pF[j][k][c];
+        } else {
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            uX[j][PA][k][c] = uF[j][k][c];
+            bX[j][PA][k][c] = bF[j][k][c];
+          }
         }
       }
-    }
     ++s;
   };
   while (s + 1 < s1) {

@@ -257,6 +257,7 @@ struct PDArgs {
   // after a P, writes u only).  rows_lo/hi[j]: rows half-step j must compute
   // (shrinking cone; cone_rows == 0 -> all rows).
   int nhalf, last, cone_rows;
+  int dbg_noproj;  // FT_PD_DEBUG_NOPROJ=1: skip the projection (timing study only, breaks parity)
   signed char rows_lo[16], rows_hi[16];
   double tau, lam, sigma, shrink;  // shrink = 1/(1+sigma*eps)
 };
@@ -450,7 +451,7 @@ __device__ __forceinline__ void pd_iterate(int iters, double *sm, int base, int 
 // of every warp running the hypot + division code for its own ~4 pairs with
 // most lanes idle).  Primal half-step: reads its p from shared memory.
 // Same arithmetic in the same order as the reference iteration.
-template <int TW, int BY, int PY, bool P2, bool IN>
+template <int TW, int BY, int PY, bool P2, bool IN, bool MID>
 __device__ __forceinline__ void pd_halfsteps_cq(const PDArgs &a, double *sm, int base, int tx,
                                                 int ty, const unsigned *fl, double *u1,
                                                 double *u2, const double *gx, const double *gy,
@@ -466,9 +467,7 @@ __device__ __forceinline__ void pd_halfsteps_cq(const PDArgs &a, double *sm, int
   const unsigned lt_mask = (1u << tx) - 1u;
   const int tid = ty * 32 + tx;
   int nd = 0;  // dual half-steps done (queue counter parity)
-  for (int j = 0; j < a.nhalf; ++j) {
-    const bool dual = ((j & 1) == 0) == (a.first != 0);
-    const int lo = a.cone_rows ? a.rows_lo[j] : 0, hi = a.cone_rows ? a.rows_hi[j] : TH;
+  auto half = [&](const bool dual, const int lo, const int hi) {
     bool row_on[NP];
     bool all = true;
 #pragma unroll
@@ -500,6 +499,7 @@ __device__ __forceinline__ void pd_halfsteps_cq(const PDArgs &a, double *sm, int
         // screening test only (not reference arithmetic): fused is fine
         if (fma(p11, p11, p12 * p12) > 0.999999) need |= 1u << (2 * q);
         if (fma(p21, p21, p22 * p22) > 0.999999) need |= 1u << (2 * q + 1);
+        if (a.dbg_noproj) need = 0;
       };
       if (all) {
 #pragma unroll
@@ -579,6 +579,20 @@ __device__ __forceinline__ void pd_halfsteps_cq(const PDArgs &a, double *sm, int
       }
     }
     __syncthreads();
+  };
+  if (MID) {
+    // middle launch (P D)x4 of a 32-row tile with halo 4: the cone rows of
+    // halfstep_schedule in closed form -- P_i: [1+i, 32-i), D_i: [1+i, 31-i)
+    static_assert(!MID || TH == 32, "closed-form cone is for 32-row tiles");
+    for (int i = 0; i < 4; ++i) {
+      half(false, 1 + i, TH - i);
+      half(true, 1 + i, TH - 1 - i);
+    }
+  } else {
+    for (int j = 0; j < a.nhalf; ++j) {
+      const bool dual = ((j & 1) == 0) == (a.first != 0);
+      half(dual, a.cone_rows ? a.rows_lo[j] : 0, a.cone_rows ? a.rows_hi[j] : TH);
+    }
   }
 }
 
@@ -599,7 +613,7 @@ struct BlockBarrier {
 };
 
 
-template <int TW, int BY, int PY, int MINB>
+template <int TW, int BY, int PY, int MINB, bool MID = false>
 __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const PDArgs a) {
   using G = PDGeom<TW, BY, PY>;
   constexpr int NX = G::NX, TH = G::TH, NP = G::NP, SP = G::SP, PL = G::PLANE;
@@ -685,7 +699,7 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const PDArgs a) {
     int *const qidx = reinterpret_cast<int *>(sm + 6 * PL);
     int *const ctr = qidx + 2 * NP * 32 * BY;
 #define FT_PD_CALL(P2_, IN_)                                                                 \
-  pd_halfsteps_cq<TW, BY, PY, P2_, IN_>(a, sm, base, tx, ty, fl, u1, u2, gx, gy, r0, thr, ig2, \
+  pd_halfsteps_cq<TW, BY, PY, P2_, IN_, MID>(a, sm, base, tx, ty, fl, u1, u2, gx, gy, r0, thr, ig2, \
                                         tl, qidx, ctr)
     if (a.pow2) {
       if (interior) FT_PD_CALL(true, true); else FT_PD_CALL(true, false);
@@ -1226,6 +1240,11 @@ __global__ void __launch_bounds__(32 * BY, 1) k_pd_persist(const PDArgs a) {
   }
 }
 
+int env_int(const char *name, int dflt) {
+  const char *v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+
 // Launch configurations (tile width x height, threads, min CTAs/SM).
 struct PDConfig {
   int idx, tw, th, by;
@@ -1234,6 +1253,7 @@ struct PDConfig {
   bool persistent = false;
   size_t smem_cq = 0;  // k_pd_tile with the CTA-wide queue (PDArgs::cq)
   bool tile = false;    // k_pd_tile: half-step schedule (PDArgs::nhalf)
+  void (*fn_mid)(PDArgs) = nullptr;  // k_pd_tile<..., MID>: middle (P D)x4 launches, halo 4
 };
 
 template <int TW, int BY, int PY>
@@ -1254,6 +1274,7 @@ PDConfig make_cfg(int idx) {
   PDConfig c{idx, TW, G::TH, BY, &k_pd_tile<TW, BY, PY, MINB>, G::smem};
   c.smem_cq = 6 * G::PLANE * sizeof(double) + (2 * G::NP * 32 * BY + 2) * sizeof(int);
   c.tile = true;
+  if (G::TH == 32) c.fn_mid = &k_pd_tile<TW, BY, PY, MINB, G::TH == 32>;
   return c;
 }
 
@@ -1279,7 +1300,7 @@ inline PDConfig pd_config(int i) {
 }
 
 int pd_launch(const PDConfig &c, const PDArgs &a, int nb, cudaStream_t s) {
-  static bool attr_done[16] = {};
+  static bool attr_done[32] = {};
   if (!attr_done[c.idx]) {
     FT_CUDA_TRY(cudaFuncSetAttribute(c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)c.smem));
@@ -1304,15 +1325,18 @@ int pd_launch(const PDConfig &c, const PDArgs &a, int nb, cudaStream_t s) {
   // the CTA-wide projection queue needs 4 B per pair instead of the per-warp
   // 16 B: smaller carve-out, larger L1
   const size_t smem = c.tile ? c.smem_cq : c.smem;
-  c.fn<<<grid, dim3(32, c.by), smem, s>>>(a);
+  const bool mid = c.fn_mid && !a.first && !a.last && a.nhalf == 8 && a.halo == 4 && a.cone_rows &&
+                   c.th == 32 && env_int("FT_PD_MID", 1);
+  if (mid && !attr_done[16 + c.idx]) {
+    FT_CUDA_TRY(cudaFuncSetAttribute(c.fn_mid, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)c.smem));
+    attr_done[16 + c.idx] = true;
+  }
+  (mid ? c.fn_mid : c.fn)<<<grid, dim3(32, c.by), smem, s>>>(a);
   count_launch();
   return FT_OK;
 }
 
-int env_int(const char *name, int dflt) {
-  const char *v = getenv(name);
-  return v && *v ? atoi(v) : dflt;
-}
 
 // k_pd_sweep launches: `nh` half-steps, starting with a dual step when
 // `first` (the warp's first launch).  pow2 time steps only (the default);
@@ -1557,6 +1581,7 @@ int profile_pd(FlowWork &fw, int w, int h, int nb, const FlowParamsD &p, int rep
   a.lam = p.lam;
   a.sigma = 1.0 / (8.0 * p.tau);
   a.shrink = 1.0 / (1.0 + a.sigma * p.eps);
+  a.dbg_noproj = env_int("FT_PD_DEBUG_NOPROJ", 0);
   cudaEvent_t e0, e1;
   FT_CUDA_TRY(cudaEventCreate(&e0));
   FT_CUDA_TRY(cudaEventCreate(&e1));
@@ -1752,6 +1777,7 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
           a.lam = p.lam;
           a.sigma = sigma;
           a.shrink = shrink;
+          a.dbg_noproj = env_int("FT_PD_DEBUG_NOPROJ", 0);
           if (sweep) FT_TRY(sweep_launch(a, n, done == 0, gn, s));
           else FT_TRY(pd_launch(plan.cfg, a, gn, s));
           cur = 1 - cur;

@@ -97,6 +97,38 @@ def test_flow_sd_tiled_matches_oracle(pkg):
     assert np.array_equal(fld.dy, want[1])
 
 
+@pytest.mark.parametrize("env", [
+    {"FT_PD_MID": "0"},                                    # generic half-step loop
+    {"FT_PD_SWEEP": "1", "FT_SWEEP_COLS": "1"},            # row-sweep, 1 column per lane
+    {"FT_PD_SWEEP": "1", "FT_SWEEP_COLS": "2"},            # row-sweep, 2 columns per lane
+    {"FT_PD_SWEEP": "1", "FT_SWEEP_COLS": "1", "FT_SWEEP_ITERS": "4", "FT_SWEEP_SEG": "24"},
+    {"FT_PD_HALO": "3"},
+    {"FT_ROF_NAIVE": "1"},
+])
+def test_flow_kernel_variants_bit_identical(pkg, env, monkeypatch):
+    """Every opt-in primal-dual / ROF kernel variant
+    gives the default path's bits on a multi-tile frame: odd sizes, several
+    segments, first / middle / last launches with the default 50 iterations."""
+    from paper_1910_06017_b200.synth import make_sequence
+    frames, _ = make_sequence(203, 141, 5, 2, seed=9)
+    im, of = pkg.imaging, pkg.optflow
+    a = im.Frame.from_gray8(frames[0])
+    b = im.Frame.from_gray8(frames[1])
+    prm = of.FlowParams(warps_per_level=1, pyramid_scales=3)
+
+    def run():
+        sa, sb = im.structure_texture(a), im.structure_texture(b)
+        f = of.compute_flow(sa, sb, prm)
+        return np.asarray(sa.data).copy(), f.dx.copy(), f.dy.copy()
+
+    base = run()
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    got = run()
+    for x, y in zip(base, got):
+        assert x.tobytes() == y.tobytes()
+
+
 def test_zero_motion_full_size(pkg):
     """Size-independent property at SD (720x576, default params): identical
     frames give an exactly zero field."""

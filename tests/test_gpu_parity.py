@@ -103,6 +103,10 @@ def test_flow_sd_tiled_matches_oracle(pkg):
     {"FT_PD_SWEEP": "1", "FT_SWEEP_COLS": "2"},            # row-sweep, 2 columns per lane
     {"FT_PD_SWEEP": "1", "FT_SWEEP_COLS": "1", "FT_SWEEP_ITERS": "4", "FT_SWEEP_SEG": "24"},
     {"FT_PD_HALO": "3"},
+    {"FT_PD_CFG": "0"},                                    # 256-thread tiles
+    {"FT_PD_CFG": "5"},                                    # register strips
+    {"FT_PD_CFG": "12"},                                   # persistent cp.async pipeline
+    {"FT_CLUSTER": "1"},                                   # cluster-resident coarse levels
     {"FT_ROF_NAIVE": "1"},
 ])
 def test_flow_kernel_variants_bit_identical(pkg, env, monkeypatch):

@@ -32,8 +32,9 @@ sys.path.insert(0, ROOT)
 
 METRIC = "tracked frames/sec per GPU at 720×576, 100 tracks; HBM-roofline fraction"
 W_, H_, N_OBJ, DET_EVERY = 720, 576, 100, 5
-WORKLOAD = ("C2: 720x576 SD, 100 tracks, scale change + occlusion, detections every 5th "
-            "frame, TV-L1 6 scales x 5 warps x 50 iterations, ROF 40 iterations, fp64")
+WORKLOAD = ("C2 streams batched as in C5 (64 SD streams per GPU): 720x576 SD, 100 tracks, "
+            "scale change + occlusion, detections every 5th frame, TV-L1 6 scales x 5 warps x "
+            "50 iterations, ROF 40 iterations, fp64")
 
 
 # ----------------------------------------------------------------------------
@@ -404,7 +405,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--streams", type=int, default=32, help="SD streams per GPU")
+    ap.add_argument("--streams", type=int, default=64,
+                    help="SD streams per GPU (64 = BASELINE config C5's stream count at N=1)")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--motion", choices=["tvl1", "klt"], default="tvl1",
                     help="tvl1: the reference path (headline); klt: SURVEY 8 f4 backend")

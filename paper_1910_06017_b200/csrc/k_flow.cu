@@ -451,7 +451,15 @@ __device__ __forceinline__ void pd_iterate(int iters, double *sm, int base, int 
 // of every warp running the hypot + division code for its own ~4 pairs with
 // most lanes idle).  Primal half-step: reads its p from shared memory.
 // Same arithmetic in the same order as the reference iteration.
-template <int TW, int BY, int PY, bool P2, bool IN, bool MID>
+// CL: the CTA is one of a 2x1 thread-block cluster covering a 64-column
+// region; the seam column is exchanged through distributed shared memory
+// after every half-step (see k_pd_tile).
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::
+                   : "memory");
+}
+
+template <int TW, int BY, int PY, bool P2, bool IN, bool MID, bool CL = false>
 __device__ __forceinline__ void pd_halfsteps_cq(const PDArgs &a, double *sm, int base, int tx,
                                                 int ty, const unsigned *fl, double *u1,
                                                 double *u2, const double *gx, const double *gy,
@@ -578,7 +586,28 @@ __device__ __forceinline__ void pd_halfsteps_cq(const PDArgs &a, double *sm, int
           if (row_on[q]) primal_px(q);
       }
     }
-    __syncthreads();
+    if (CL) {
+      // seam exchange: after a primal step the right CTA's column 0 u-bar
+      // goes to the left CTA's right apron; after a dual step (projection
+      // done: block barrier first) the left CTA's column 31 (p11, p21) goes
+      // to the right CTA's left apron.  The cluster barrier publishes them.
+      static_assert(!CL || TW == 32, "seam exchange assumes 32-column tiles");
+      cg::cluster_group cl = cg::this_cluster();
+      const unsigned rank = cl.block_rank();
+      if (dual) __syncthreads();
+      if (dual ? (rank == 0 && tx == 31) : (rank == 1 && tx == 0)) {
+        double2 *const plane = dual ? sPX : sB;
+        double2 *const remote = cl.map_shared_rank(plane, rank ^ 1u);
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+          const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
+          remote[id + (dual ? -31 : 31) + (dual ? -1 : 1)] = plane[id];
+        }
+      }
+      cluster_sync_all();
+    } else {
+      __syncthreads();
+    }
   };
   if (MID) {
     // middle launch (P D)x4 of a 32-row tile with halo 4: the cone rows of
@@ -613,7 +642,7 @@ struct BlockBarrier {
 };
 
 
-template <int TW, int BY, int PY, int MINB, bool MID = false>
+template <int TW, int BY, int PY, int MINB, bool MID = false, bool CL = false>
 __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const PDArgs a) {
   using G = PDGeom<TW, BY, PY>;
   constexpr int NX = G::NX, TH = G::TH, NP = G::NP, SP = G::SP, PL = G::PLANE;
@@ -621,7 +650,11 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const PDArgs a) {
 
   const int W = a.w, H = a.h;
   const int step_x = TW - 2 * a.halo, step_y = TH - 2 * a.halo;
-  const int ox = blockIdx.x * step_x - a.halo;
+  // CL: 2x1 cluster over a (2 TW)-column region with the halo on its outer
+  // sides only; rank 0 is the left tile, rank 1 the right one
+  const int rk = CL ? (int)(blockIdx.x & 1) : 0;
+  const int ox = CL ? (int)(blockIdx.x >> 1) * (2 * TW - 2 * a.halo) - a.halo + TW * rk
+                    : (int)blockIdx.x * step_x - a.halo;
   const int oy = blockIdx.y * step_y - a.halo;
   const int64_t so = blockIdx.z * a.cap;
   const int tx = threadIdx.x, ty = threadIdx.y;
@@ -637,6 +670,29 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const PDArgs a) {
     else idx = (k - 2 * SP - TH + 1) * SP + SP - 1;
 #pragma unroll
     for (int f = 0; f < 6; ++f) sm[sxi(f, idx, PL)] = 0.0;
+  }
+  if (CL) {
+    // seam apron before the first half-step (later ones are pushed by the
+    // neighbour): the right tile's first primal step reads (p11, p21) at
+    // column ox-1; the left tile's first dual step (first launch) reads
+    // u-bar = u at column ox+TW
+    __syncthreads();  // after the apron zeroing
+    const bool need = rk == 1 ? (!a.first && tx == 0) : (a.first && tx == 31);
+    if (need) {
+      const int gc = rk == 1 ? ox - 1 : ox + TW;
+#pragma unroll
+      for (int k = 0; k < PY; ++k) {
+        const int lr = ty + BY * k, gr = oy + lr;
+        const bool in = gc >= 0 && gc < W && gr >= 0 && gr < H;
+        const int64_t o = so + (int64_t)gr * W + gc;
+        const int idx = (lr + 1) * SP + (rk == 1 ? 0 : SP - 1);
+        const int f0 = rk == 1 ? 2 : 0, f1 = rk == 1 ? 4 : 1;  // (p11, p21) / (b1, b2)
+        const double *s0 = rk == 1 ? a.in.p[P11] : a.in.p[U1];
+        const double *s1 = rk == 1 ? a.in.p[P21] : a.in.p[U2];
+        sm[sxi(f0, idx, PL)] = in ? s0[o] : 0.0;
+        sm[sxi(f1, idx, PL)] = in ? s1[o] : 0.0;
+      }
+    }
   }
 
   const double tl = a.tau * a.lam;
@@ -699,7 +755,7 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const PDArgs a) {
     int *const qidx = reinterpret_cast<int *>(sm + 6 * PL);
     int *const ctr = qidx + 2 * NP * 32 * BY;
 #define FT_PD_CALL(P2_, IN_)                                                                 \
-  pd_halfsteps_cq<TW, BY, PY, P2_, IN_, MID>(a, sm, base, tx, ty, fl, u1, u2, gx, gy, r0, thr, ig2, \
+  pd_halfsteps_cq<TW, BY, PY, P2_, IN_, MID, CL>(a, sm, base, tx, ty, fl, u1, u2, gx, gy, r0, thr, ig2, \
                                         tl, qidx, ctr)
     if (a.pow2) {
       if (interior) FT_PD_CALL(true, true); else FT_PD_CALL(true, false);
@@ -711,7 +767,7 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const PDArgs a) {
 
   // ---- write back the exact interior: u, and p unless this is the warp's
   // last launch (the next warp starts from p = 0)
-  const int lo_x = a.halo, hi_x = TW - a.halo;
+  const int lo_x = (CL && rk == 1) ? 0 : a.halo, hi_x = (CL && rk == 0) ? TW : TW - a.halo;
   const int lo_y = a.halo, hi_y = TH - a.halo;
 #pragma unroll
   for (int q = 0; q < NP; ++q) {
@@ -1254,6 +1310,8 @@ struct PDConfig {
   size_t smem_cq = 0;  // k_pd_tile with the CTA-wide queue (PDArgs::cq)
   bool tile = false;    // k_pd_tile: half-step schedule (PDArgs::nhalf)
   void (*fn_mid)(PDArgs) = nullptr;  // k_pd_tile<..., MID>: middle (P D)x4 launches, halo 4
+  void (*fn_cl)(PDArgs) = nullptr;   // 2x1 cluster variants (FT_PD_CL=1)
+  void (*fn_mid_cl)(PDArgs) = nullptr;
 };
 
 template <int TW, int BY, int PY>
@@ -1275,6 +1333,10 @@ PDConfig make_cfg(int idx) {
   c.smem_cq = 6 * G::PLANE * sizeof(double) + (2 * G::NP * 32 * BY + 2) * sizeof(int);
   c.tile = true;
   if (G::TH == 32) c.fn_mid = &k_pd_tile<TW, BY, PY, MINB, G::TH == 32>;
+  if (TW == 32 && G::TH == 32 && BY == 16) {
+    c.fn_cl = &k_pd_tile<TW, BY, PY, MINB, false, TW == 32 && BY == 16>;
+    c.fn_mid_cl = &k_pd_tile<TW, BY, PY, MINB, G::TH == 32, TW == 32 && BY == 16>;
+  }
   return c;
 }
 
@@ -1331,6 +1393,31 @@ int pd_launch(const PDConfig &c, const PDArgs &a, int nb, cudaStream_t s) {
     FT_CUDA_TRY(cudaFuncSetAttribute(c.fn_mid, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)c.smem));
     attr_done[16 + c.idx] = true;
+  }
+  if (c.fn_cl && a.halo > 0 && env_int("FT_PD_CL", 0)) {
+    void (*fn)(PDArgs) = mid ? c.fn_mid_cl : c.fn_cl;
+    static void (*cl_attr[4])(PDArgs) = {};
+    const int ck = (mid ? 1 : 0);
+    if (cl_attr[ck] != fn) {
+      FT_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem));
+      cl_attr[ck] = fn;
+    }
+    const int rx = 2 * c.tw - 2 * a.halo;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * ((a.w + rx - 1) / rx), grid.y, grid.z);
+    cfg.blockDim = dim3(32, c.by);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    FT_CUDA_TRY(cudaLaunchKernelEx(&cfg, fn, a));
+    count_launch();
+    return FT_OK;
   }
   (mid ? c.fn_mid : c.fn)<<<grid, dim3(32, c.by), smem, s>>>(a);
   count_launch();

@@ -107,6 +107,7 @@ def test_flow_sd_tiled_matches_oracle(pkg):
     {"FT_PD_CFG": "5"},                                    # register strips
     {"FT_PD_CFG": "12"},                                   # persistent cp.async pipeline
     {"FT_CLUSTER": "1"},                                   # cluster-resident coarse levels
+    {"FT_PD_CL": "1"},                                     # 2x1 clusters sharing the seam
     {"FT_ROF_NAIVE": "1"},
 ])
 def test_flow_kernel_variants_bit_identical(pkg, env, monkeypatch):

@@ -32,9 +32,33 @@ sys.path.insert(0, ROOT)
 
 METRIC = "tracked frames/sec per GPU at 720×576, 100 tracks; HBM-roofline fraction"
 W_, H_, N_OBJ, DET_EVERY = 720, 576, 100, 5
+SCALES = None  # FlowParams.pyramid_scales (None: auto_scales, 6 at SD)
 WORKLOAD = ("C2 streams batched as in C5 (64 SD streams per GPU): 720x576 SD, 100 tracks, "
             "scale change + occlusion, detections every 5th frame, TV-L1 6 scales x 5 warps x "
             "50 iterations, ROF 40 iterations, fp64")
+# BASELINE.json configs other than the headline, as measured (non-headline)
+# lines: (W, H, tracks, detector cadence, pyramid scales, algorithmic bytes /
+# frame from SURVEY 8(d), workload text)
+CONFIGS = {
+    "c2": None,
+    "c3": (1920, 1080, 200, 1, 4, 27.47e9,
+           "C3: 1920x1080 HD (processed at level 1, 960x540), 200 tracks, detections every "
+           "frame, TV-L1 4 scales x 5 warps x 50 iterations, ROF 40 iterations, fp64"),
+    "c4": (3840, 2160, 500, 1, 5, 27.69e9,
+           "C4: 3840x2160 UHD (processed at level 2, 960x540), 500 tracks, detections every "
+           "frame, TV-L1 5 scales x 5 warps x 50 iterations, ROF 40 iterations, fp64 "
+           "(the KLT forward-backward check has no counterpart on the reference path)"),
+}
+
+
+def apply_config(name: str) -> None:
+    global W_, H_, N_OBJ, DET_EVERY, SCALES, WORKLOAD, METRIC
+    c = CONFIGS.get(name)
+    if c is None:
+        return
+    W_, H_, N_OBJ, DET_EVERY, SCALES, fb, WORKLOAD = c
+    FRAME_BYTES["default"] = fb
+    METRIC = f"tracked frames/sec per GPU at {W_}×{H_}, {N_OBJ} tracks; HBM-roofline fraction"
 
 
 # ----------------------------------------------------------------------------
@@ -165,14 +189,17 @@ def _flow_params(flow: str, oracle: bool = False):
         cls = O.FlowParams
     else:
         from paper_1910_06017_b200.optflow import FlowParams as cls
-    return cls() if flow == "default" else cls(warps_per_level=2, iterations_per_warp=10)
+    if flow == "default":
+        return cls(pyramid_scales=SCALES)
+    return cls(warps_per_level=2, iterations_per_warp=10, pyramid_scales=SCALES)
 
 
 FRAME_BYTES = {"default": 22.03e9, "light": 2.52e9}  # SURVEY 8(d) algorithmic bytes / SD frame
 
 
 def _cpu_frame_job(args):
-    rank, s, flow = args
+    rank, s, flow, config = args
+    apply_config(config)  # spawned child: module globals start at the headline config
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     from oracle import ftoracle as O
     from paper_1910_06017_b200.synth import make_sequence
@@ -188,13 +215,13 @@ def _cpu_frame_job(args):
     return time.perf_counter() - t0
 
 
-def cpu_run(n_procs: int, jobs: int, flow: str = "default"):
+def cpu_run(n_procs: int, jobs: int, flow: str = "default", config: str = "c2"):
     for var in ("OMP_NUM_THREADS", "MKL_NUM_THREADS", "OPENBLAS_NUM_THREADS"):
         os.environ[var] = "1"  # one core per process (children inherit)
     ctx = mp.get_context("spawn")
     t0 = time.perf_counter()
     with ctx.Pool(n_procs) as pool:
-        per = pool.map(_cpu_frame_job, [(99, s, flow) for s in range(jobs)])
+        per = pool.map(_cpu_frame_job, [(99, s, flow, config) for s in range(jobs)])
     return time.perf_counter() - t0, per
 
 
@@ -205,14 +232,14 @@ def host_cores() -> int:
         return os.cpu_count() or 1
 
 
-def cpu_baseline_measure(flow: str = "default"):
+def cpu_baseline_measure(flow: str = "default", config: str = "c2"):
     cores = host_cores()
-    wall, per = cpu_run(cores, cores, flow)
+    wall, per = cpu_run(cores, cores, flow, config)
     # each process measured its own tracked frame; aggregate = cores / mean
     per_core_fps = 1.0 / float(np.mean(per))
     return {"value": round(per_core_fps * cores, 5), "unit": "frames/s", "cores": cores,
             "kind": "port", "per_core_fps": round(per_core_fps, 5),
-            "sample": f"{cores} processes x 1 tracked SD frame (C2 workload, 100 tracks, {flow} "
+            "sample": f"{cores} processes x 1 tracked frame ({config} workload, {N_OBJ} tracks, {flow} "
                       f"FlowParams) through oracle/ftoracle.py (numpy restatement of the "
                       f"reference, bit-exact); wall {wall:.1f}s"}
 
@@ -224,7 +251,7 @@ def run_reference(args, ws, rank):
     # warm-up: import + a tiny step per process (numpy has no JIT; keeps W semantics)
     step_times = []
     for k in range(args.steps):
-        wall, per = cpu_run(cores, cores, args.flow)
+        wall, per = cpu_run(cores, cores, args.flow, args.config)
         step_times.append(wall)
         if sum(step_times) > args.ref_budget_s:
             break
@@ -259,7 +286,7 @@ def run_ours(args, ws, rank, local):
     dev = torch.device("cuda", local)
     B, K, Wm = args.streams, args.steps, args.warmup
     T = Wm + K + 1
-    max_tracks, max_dets = 256, 160
+    max_tracks, max_dets = max(256, 2 * N_OBJ + 56), max(160, N_OBJ + 60)
     seqs = gen_streams(rank, B, T)
     frames = np.stack([np.stack([seqs[s][0][t] for s in range(B)]) for t in range(T)])  # T,B,H,W
     dets = np.zeros((T, B, max_dets), dtype=_lib.DET_DTYPE)
@@ -322,7 +349,9 @@ def run_ours(args, ws, rank, local):
         # ncu capture of one finest-level launch, normalised per stream-pixel
         # and rescaled to this run's streams (same kernel, same geometry)
         if tj.get("bytes_per_stream_pixel"):
-            traffic = round(tj["bytes_per_stream_pixel"] * B * W_ * H_, 1)
+            from paper_1910_06017_b200.imaging import select_level
+            lv = select_level(W_, H_)  # the flow runs at the processing level
+            traffic = round(tj["bytes_per_stream_pixel"] * B * (W_ >> lv) * (H_ >> lv), 1)
     # step-level roofline: SURVEY 8(d) algorithmic bytes per SD frame (22.03 GB at C2)
     frame_bytes = FRAME_BYTES[args.flow]
     step_frac = (value / ws) * frame_bytes / (hbm * 1e9)
@@ -354,7 +383,7 @@ def run_ours(args, ws, rank, local):
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_measure(args.flow)
+        cpu = cpu_baseline_measure(args.flow, args.config)
 
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 3), "unit": "frames/s", "n_gpus": ws,
@@ -414,7 +443,10 @@ def main():
                     help="default FlowParams (headline) or SURVEY 8(d)'s light 2 warps x 10 iters")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget-s", type=float, default=150.0)
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2",
+                    help="c2 (headline) or another BASELINE.json config as a non-headline line")
     args = ap.parse_args()
+    apply_config(args.config)
     ws, rank, local = dist_init()
     if args.impl == "reference":
         run_reference(args, ws, rank)

@@ -200,13 +200,16 @@ __global__ void k_st_combine(const double *__restrict__ img, int w, int h, int64
 constexpr int kRTW = 32, kRBY = 16, kRPY = 2, kRTH = kRBY * kRPY;
 constexpr int kRSP = kRTW + 2, kRPL = kRSP * (kRTH + 2);
 
-template <bool P2>
+// FIX: halo 4 with 4 iterations per launch (every launch of the default 40
+// iterations): trip count and cone rows are compile-time constants.
+template <bool P2, bool FIX = false>
 __global__ void __launch_bounds__(32 * kRBY, 2)
     k_rof_tile(const double *__restrict__ img, int w, int h, int64_t is,
                const double *__restrict__ px_in, const double *__restrict__ py_in,
                double *__restrict__ px_out, double *__restrict__ py_out, int64_t ps,
                double weight, double step, int halo, int iters, int first, int cone_on) {
   __shared__ double s_px[kRPL], s_py[kRPL], s_d[kRPL];
+  if (FIX) halo = iters = 4;
   const int step_x = kRTW - 2 * halo, step_y = kRTH - 2 * halo;
   const int ox = blockIdx.x * step_x - halo, oy = blockIdx.y * step_y - halo;
   img += blockIdx.z * is;
@@ -242,8 +245,9 @@ __global__ void __launch_bounds__(32 * kRBY, 2)
   // Shrinking cone (tiles with a halo): iteration it (0-based) needs p on
   // rows [c+it+1, TH-c-it-1) and d on [c+it+1, TH-c-it), c = halo - iters,
   // for the written interior [halo, TH-halo); a row is one warp.
-  const int cone = (cone_on && halo > 0 && iters <= halo) ? halo - iters : -1;
-  for (int it = 0; it < iters; ++it) {
+  const int cone = FIX ? 0 : (cone_on && halo > 0 && iters <= halo) ? halo - iters : -1;
+#pragma unroll
+  for (int it = 0; it < (FIX ? 4 : iters); ++it) {
     double d[kRPY];
 #pragma unroll
     for (int k = 0; k < kRPY; ++k) {  // d = divergence(p) - img/weight
@@ -284,6 +288,11 @@ __global__ void __launch_bounds__(32 * kRBY, 2)
     px_out[o] = px[k];
     py_out[o] = py[k];
   }
+}
+
+int getenv_int(const char *name, int dflt) {
+  const char *v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
 }
 
 int grid1d(int64_t n, int bs) {
@@ -361,7 +370,9 @@ int launch_structure_texture(const double *img, int w, int h, int64_t is, double
       const int k = resident ? iterations : std::min(halo, iterations - done);
       int e2 = 0;
       const bool p2 = step > 0.0 && std::frexp(step, &e2) == 0.5;
-      auto kern = p2 ? k_rof_tile<true> : k_rof_tile<false>;
+      const bool fix = !resident && halo == 4 && k == 4 && cone_on && getenv_int("FT_ROF_FIX", 1);
+      auto kern = p2 ? (fix ? k_rof_tile<true, true> : k_rof_tile<true>)
+                     : (fix ? k_rof_tile<false, true> : k_rof_tile<false>);
       kern<<<g, dim3(32, kRBY), 0, s>>>(img, w, h, is, p[cur][0], p[cur][1], p[1 - cur][0],
                                         p[1 - cur][1], wss, weight, step, halo, k, done == 0,
                                         cone_on);

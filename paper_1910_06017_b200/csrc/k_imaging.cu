@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <type_traits>
 
 #include "ft_internal.cuh"
 
@@ -290,6 +291,176 @@ __global__ void __launch_bounds__(32 * kRBY, 2)
   }
 }
 
+// ROF row sweep (opt-in FT_ROF_SWEEP=1), the k_pd_sweep scheme applied to
+// the ROF dual iteration (imaging.py:120-124): one warp owns a 32-column
+// strip (lane = column, K halo columns per side) and a row segment, and
+// streams down the rows with the 2K half-steps of K iterations pipelined at
+// one-row lags -- stage 2k (A_k): d = div(p) - img/weight; stage 2k+1 (B_k):
+// p = (p + step*grad d) / (1 + step*|grad d|).  A stages run before B stages
+// within a step, so all stages of a step are independent; x neighbours by
+// shuffles, y neighbours from the lane's previous rows (register carries,
+// two alternating slots); rows clipped per stage to the segment's cone.
+// Every pixel needs hypot + two divisions, so no queue: no barriers at all.
+__device__ __forceinline__ void rof_cp8(double *dst, const double *src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 8 : 0));
+}
+
+struct RofSweepArgs {
+  const double *img;
+  int w, h;
+  int64_t is;
+  const double *px_in, *py_in;
+  double *px_out, *py_out;
+  int64_t ps;
+  double weight, step;
+  int first, seg;
+  signed char cA[16], cB[16];
+};
+
+template <bool P2, int K>
+__global__ void __launch_bounds__(32, 16) k_rof_sweep(const RofSweepArgs a) {
+  constexpr int NH = 2 * K, L = NH - 1, NSLOT = 4, PF = NSLOT - 3, CR = 8;
+  constexpr int STRIP = 32 - 2 * K;
+  static_assert(NH - 2 < CR, "iw ring too short");
+  __shared__ double ring[NSLOT][3][32];  // img, px, py of rows s-1 .. s+1+PF
+  __shared__ double iwr[CR][32];         // img/weight of the rows A stages read
+  const int lane = threadIdx.x;
+  const int W = a.w, H = a.h;
+  const int x = blockIdx.x * STRIP - K + lane;
+  const bool xin = x >= 0 && x < W;
+  const bool wr = xin && lane >= K && lane < 32 - K;
+  const bool fR = x < W - 1, fL = x > 0, fLC = x == W - 1;
+  const int y0 = blockIdx.y * a.seg, y1 = min(y0 + a.seg, H);
+  const double *img = a.img + blockIdx.z * a.is;
+  const int64_t po = blockIdx.z * a.ps;
+  const double step = a.step, weight = a.weight;
+  int lo[NH], hi[NH], s1 = 0;
+#pragma unroll
+  for (int j = 0; j < NH; ++j) {
+    lo[j] = max(y0 - (int)a.cA[j], 0);
+    hi[j] = min(y1 + (int)a.cB[j], H);
+    s1 = max(s1, hi[j] + j);
+  }
+  const int s0 = lo[0];
+  const int lr0 = max(lo[0] - 1, 0), lr1 = min(hi[0] + 1, H);
+  auto load_row = [&](int r) {
+    if (r < lr0 || r >= lr1) return;
+    const int sl = r & (NSLOT - 1);
+    const int64_t o = (int64_t)r * W + x;
+    rof_cp8(&ring[sl][0][lane], xin ? img + o : img, xin);
+    if (!a.first) {
+      rof_cp8(&ring[sl][1][lane], xin ? a.px_in + po + o : a.px_in, xin);
+      rof_cp8(&ring[sl][2][lane], xin ? a.py_in + po + o : a.py_in, xin);
+    }
+  };
+  auto rd = [&](int r, int f) -> double {
+    return (a.first && f) ? 0.0 : ring[r & (NSLOT - 1)][f][lane];
+  };
+  auto iw_row = [&](int r) { iwr[r & (CR - 1)][lane] = rd(r, 0) / weight; };  // imaging.py:121
+  load_row(s0 - 1);
+  load_row(s0);
+  load_row(s0 + 1);
+  asm volatile("cp.async.commit_group;\n" ::);
+  // carries: slot t = rows produced at steps with (s - s0) & 1 == t
+  double pX[K][2][2], dX[K][2];
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+#pragma unroll
+    for (int t = 0; t < 2; ++t) pX[k][t][0] = pX[k][t][1] = dX[k][t] = 0.0;
+  int s = s0;
+  auto stepf = [&](auto slot) {
+    constexpr int PA = decltype(slot)::value, PB = PA ^ 1;
+    load_row(s + 1 + PF);
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(PF) : "memory");
+    if (s == s0 && s0 < lr1) iw_row(s0);
+    double dF[K];
+    // ---- A stages: d = div(p) - img/weight at rows s - 2k
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int r = s - 2 * k;
+      double p1, p2, q2;  // px(r), py(r), py(r-1)
+      if (k == 0) {
+        p1 = rd(r, 1); p2 = rd(r, 2); q2 = rd(r - 1, 2);
+      } else {
+        p1 = pX[k - 1][PB][0]; p2 = pX[k - 1][PB][1]; q2 = pX[k - 1][PA][1];
+      }
+      const double l1 = __shfl_up_sync(0xffffffffu, p1, 1);
+      const bool U = r > 0, LR = r == H - 1;
+      const double dx = fL ? (fLC ? -l1 : p1 - l1) : p1;
+      const double dy = U ? (LR ? -q2 : p2 - q2) : p2;
+      dF[k] = (dx + dy) - iwr[r & (CR - 1)][lane];
+    }
+    if (s + 1 < lr1) iw_row(s + 1);
+    double pF[K][2];
+    // ---- B stages: p update at rows s - 2k - 1
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int r = s - 2 * k - 1;
+      const double dc = dX[k][PB], dd = dF[k];  // d(r), d(r+1)
+      const double dr = __shfl_down_sync(0xffffffffu, dc, 1);
+      double o1, o2;  // own p before the update
+      if (k == 0) { o1 = rd(r, 1); o2 = rd(r, 2); }
+      else { o1 = pX[k - 1][PA][0]; o2 = pX[k - 1][PA][1]; }
+      const bool D = r < H - 1;
+      const double gx = fR ? dr - dc : 0.0;
+      const double gy = D ? dd - dc : 0.0;
+      const double hy = glibc_hypot(gx, gy);
+      const double norm = P2 ? fma(step, hy, 1.0) : 1.0 + step * hy;
+      pF[k][0] = (P2 ? fma(step, gx, o1) : o1 + step * gx) / norm;
+      pF[k][1] = (P2 ? fma(step, gy, o2) : o2 + step * gy) / norm;
+    }
+    {
+      const int r = s - L;
+      if (r >= y0 && r < y1 && wr) {
+        const int64_t o = po + (int64_t)r * W + x;
+        a.px_out[o] = pF[K - 1][0];
+        a.py_out[o] = pF[K - 1][1];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      dX[k][PA] = dF[k];
+      pX[k][PA][0] = pF[k][0];
+      pX[k][PA][1] = pF[k][1];
+    }
+    ++s;
+  };
+  while (s + 1 < s1) {
+    stepf(std::integral_constant<int, 0>{});
+    stepf(std::integral_constant<int, 1>{});
+  }
+  if (s < s1) stepf(std::integral_constant<int, 0>{});
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+// stage cone of a (A B)xK sweep launch: B at [a,b) reads A at [a,b+1) and the
+// previous B at [a,b); A at [a,b) reads the previous B at [a-1,b)
+void rof_cone(int nh, signed char *cA, signed char *cB) {
+  int A[16], B[16];
+  for (int j = 0; j < 16; ++j) A[j] = B[j] = -1000;
+  auto cover = [&](int j, int x, int y) {
+    if (j < 0) return;
+    A[j] = std::max(A[j], x);
+    B[j] = std::max(B[j], y);
+  };
+  cover(nh - 1, 0, 0);
+  for (int j = nh - 1; j >= 0; --j) {
+    if (A[j] == -1000) continue;
+    if (j & 1) {
+      cover(j - 1, A[j], B[j] + 1);
+      cover(j - 2, A[j], B[j]);
+    } else {
+      cover(j - 1, A[j] + 1, B[j]);
+    }
+  }
+  for (int j = 0; j < 16; ++j) {
+    cA[j] = (signed char)(j < nh ? std::max(A[j], 0) : 0);
+    cB[j] = (signed char)(j < nh ? std::max(B[j], 0) : 0);
+  }
+}
+
 int getenv_int(const char *name, int dflt) {
   const char *v = getenv(name);
   return v && *v ? atoi(v) : dflt;
@@ -370,6 +541,30 @@ int launch_structure_texture(const double *img, int w, int h, int64_t is, double
       const int k = resident ? iterations : std::min(halo, iterations - done);
       int e2 = 0;
       const bool p2 = step > 0.0 && std::frexp(step, &e2) == 0.5;
+      if (!resident && k == 4 && getenv_int("FT_ROF_SWEEP", 0)) {
+        RofSweepArgs ra;
+        ra.img = img;
+        ra.w = w;
+        ra.h = h;
+        ra.is = is;
+        ra.px_in = p[cur][0];
+        ra.py_in = p[cur][1];
+        ra.px_out = p[1 - cur][0];
+        ra.py_out = p[1 - cur][1];
+        ra.ps = wss;
+        ra.weight = weight;
+        ra.step = step;
+        ra.first = done == 0;
+        ra.seg = std::max(1, getenv_int("FT_ROF_SWEEP_SEG", 64));
+        rof_cone(8, ra.cA, ra.cB);
+        const dim3 gs((w + 23) / 24, (h + ra.seg - 1) / ra.seg, nb);
+        if (p2) k_rof_sweep<true, 4><<<gs, 32, 0, s>>>(ra);
+        else k_rof_sweep<false, 4><<<gs, 32, 0, s>>>(ra);
+        count_launch();
+        cur = 1 - cur;
+        done += k;
+        continue;
+      }
       const bool fix = !resident && halo == 4 && k == 4 && cone_on && getenv_int("FT_ROF_FIX", 1);
       auto kern = p2 ? (fix ? k_rof_tile<true, true> : k_rof_tile<true>)
                      : (fix ? k_rof_tile<false, true> : k_rof_tile<false>);

@@ -198,18 +198,25 @@ __global__ void k_st_combine(const double *__restrict__ img, int w, int h, int64
 // read at a neighbour (p at x-1 / y-1 for the divergence, d at x+1 / y+1 for
 // the forward gradient) live in shared memory with a one-element apron,
 // img/weight and the own p in registers.  Exact inner region written back.
-constexpr int kRTW = 32, kRBY = 16, kRPY = 2, kRTH = kRBY * kRPY;
-constexpr int kRSP = kRTW + 2, kRPL = kRSP * (kRTH + 2);
+constexpr int kRTW = 32, kRPY = 2, kRSP = kRTW + 2;
+// BY warps per CTA: 16 (32x32 tiles, 2 CTAs/SM) or 32 (32x64 tiles, one CTA)
+template <int BY>
+struct RofGeom {
+  static constexpr int TH = BY * kRPY, PL = kRSP * (TH + 2);
+  static constexpr size_t smem = 3 * PL * sizeof(double);
+};
 
 // FIX: halo 4 with 4 iterations per launch (every launch of the default 40
 // iterations): trip count and cone rows are compile-time constants.
-template <bool P2, bool FIX = false>
-__global__ void __launch_bounds__(32 * kRBY, 2)
+template <bool P2, bool FIX = false, int kRBY = 16>
+__global__ void __launch_bounds__(32 * kRBY, kRBY == 16 ? 2 : 1)
     k_rof_tile(const double *__restrict__ img, int w, int h, int64_t is,
                const double *__restrict__ px_in, const double *__restrict__ py_in,
                double *__restrict__ px_out, double *__restrict__ py_out, int64_t ps,
                double weight, double step, int halo, int iters, int first, int cone_on) {
-  __shared__ double s_px[kRPL], s_py[kRPL], s_d[kRPL];
+  constexpr int kRTH = RofGeom<kRBY>::TH, kRPL = RofGeom<kRBY>::PL;
+  extern __shared__ double rof_sm[];
+  double *const s_px = rof_sm, *const s_py = rof_sm + kRPL, *const s_d = rof_sm + 2 * kRPL;
   if (FIX) halo = iters = 4;
   const int step_x = kRTW - 2 * halo, step_y = kRTH - 2 * halo;
   const int ox = blockIdx.x * step_x - halo, oy = blockIdx.y * step_y - halo;
@@ -530,6 +537,8 @@ int launch_structure_texture(const double *img, int w, int h, int64_t is, double
   } else {
     const char *hv = getenv("FT_ROF_HALO");
     const int halo_t = (hv && *hv) ? atoi(hv) : 4;
+    const int tall = getenv_int("FT_ROF_TALL", 0);  // 32x64 tiles, 1024 threads
+    const int kRTH = tall ? RofGeom<32>::TH : RofGeom<16>::TH;
     const bool resident = w <= kRTW && h <= kRTH;
     const int halo = resident ? 0 : halo_t;
     const char *cv = getenv("FT_ROF_CONE");
@@ -566,9 +575,14 @@ int launch_structure_texture(const double *img, int w, int h, int64_t is, double
         continue;
       }
       const bool fix = !resident && halo == 4 && k == 4 && cone_on && getenv_int("FT_ROF_FIX", 1);
-      auto kern = p2 ? (fix ? k_rof_tile<true, true> : k_rof_tile<true>)
-                     : (fix ? k_rof_tile<false, true> : k_rof_tile<false>);
-      kern<<<g, dim3(32, kRBY), 0, s>>>(img, w, h, is, p[cur][0], p[cur][1], p[1 - cur][0],
+      auto kern = tall ? (p2 ? (fix ? k_rof_tile<true, true, 32> : k_rof_tile<true, false, 32>)
+                             : (fix ? k_rof_tile<false, true, 32> : k_rof_tile<false, false, 32>))
+                       : (p2 ? (fix ? k_rof_tile<true, true> : k_rof_tile<true>)
+                             : (fix ? k_rof_tile<false, true> : k_rof_tile<false>));
+      const size_t rsm = tall ? RofGeom<32>::smem : RofGeom<16>::smem;
+      if (rsm > 48 * 1024)
+        FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
+      kern<<<g, dim3(32, tall ? 32 : 16), rsm, s>>>(img, w, h, is, p[cur][0], p[cur][1], p[1 - cur][0],
                                         p[1 - cur][1], wss, weight, step, halo, k, done == 0,
                                         cone_on);
       count_launch();

@@ -257,7 +257,6 @@ struct PDArgs {
   // after a P, writes u only).  rows_lo/hi[j]: rows half-step j must compute
   // (shrinking cone; cone_rows == 0 -> all rows).
   int nhalf, last, cone_rows;
-  int dbg_noproj;  // FT_PD_DEBUG_NOPROJ=1: skip the projection (timing study only, breaks parity)
   signed char rows_lo[16], rows_hi[16];
   double tau, lam, sigma, shrink;  // shrink = 1/(1+sigma*eps)
 };
@@ -507,7 +506,9 @@ __device__ __forceinline__ void pd_halfsteps_cq(const PDArgs &a, double *sm, int
         // screening test only (not reference arithmetic): fused is fine
         if (fma(p11, p11, p12 * p12) > 0.999999) need |= 1u << (2 * q);
         if (fma(p21, p21, p22 * p22) > 0.999999) need |= 1u << (2 * q + 1);
-        if (a.dbg_noproj) need = 0;
+#ifdef FT_PD_DEBUG_NOPROJ
+        need = 0;  // timing study only: skip the projection (breaks parity)
+#endif
       };
       if (all) {
 #pragma unroll
@@ -1668,7 +1669,6 @@ int profile_pd(FlowWork &fw, int w, int h, int nb, const FlowParamsD &p, int rep
   a.lam = p.lam;
   a.sigma = 1.0 / (8.0 * p.tau);
   a.shrink = 1.0 / (1.0 + a.sigma * p.eps);
-  a.dbg_noproj = env_int("FT_PD_DEBUG_NOPROJ", 0);
   cudaEvent_t e0, e1;
   FT_CUDA_TRY(cudaEventCreate(&e0));
   FT_CUDA_TRY(cudaEventCreate(&e1));
@@ -1864,7 +1864,6 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
           a.lam = p.lam;
           a.sigma = sigma;
           a.shrink = shrink;
-          a.dbg_noproj = env_int("FT_PD_DEBUG_NOPROJ", 0);
           if (sweep) FT_TRY(sweep_launch(a, n, done == 0, gn, s));
           else FT_TRY(pd_launch(plan.cfg, a, gn, s));
           cur = 1 - cur;

@@ -97,8 +97,37 @@ def test_flow_sd_tiled_matches_oracle(pkg):
     assert np.array_equal(fld.dy, want[1])
 
 
+@pytest.mark.parametrize("w,h,scales", [
+    (2, 2, 1),      # smallest frame the pyramid accepts
+    (17, 3, 1),     # one partial tile row
+    (33, 31, 2),    # one column past a 32-wide tile, one row short of it
+    (31, 97, 3),    # tall and narrow: ragged in both directions at every level
+    (129, 65, 4),   # one past 4 tiles wide, 1 past 2 tiles high
+])
+def test_flow_ragged_sizes_match_oracle(pkg, w, h, scales):
+    """Ragged / tiny frames (partial tiles at every pyramid level, the
+    reference's 2x2 minimum) against the oracle with the default FlowParams
+    apart from the scale count.  On these exact inputs the oracle equals the
+    live reference bit for bit (checked in the container, where
+    /root/reference exists)."""
+    from oracle import ftoracle as O
+    rng = np.random.default_rng(w * 1000 + h)
+    u8a = rng.integers(0, 256, (h, w), dtype=np.uint8)
+    u8b = np.roll(u8a, (1, -1), axis=(0, 1))
+    sa = O.structure_texture(O.gray8_to_unit(u8a))
+    sb = O.structure_texture(O.gray8_to_unit(u8b))
+    want = O.compute_flow(sa, sb, O.FlowParams(pyramid_scales=scales))
+    of, im = pkg.optflow, pkg.imaging
+    dst = im.structure_texture(im.Frame.from_gray8(u8b)).data
+    assert np.array_equal(dst, sb)
+    fld = of.compute_flow(im.Frame.from_array(sa), im.Frame.from_array(sb),
+                          of.FlowParams(pyramid_scales=scales))
+    assert np.array_equal(fld.dx, want[0])
+    assert np.array_equal(fld.dy, want[1])
+
+
 @pytest.mark.parametrize("env", [
-    {"FT_PD_MID": "0"},                                    # generic half-step loop
+    {"FT_PD_MID": "0"},                                   # generic half-step loop
     {"FT_PD_SWEEP": "1", "FT_SWEEP_COLS": "1"},            # row-sweep, 1 column per lane
     {"FT_PD_SWEEP": "1", "FT_SWEEP_COLS": "2"},            # row-sweep, 2 columns per lane
     {"FT_PD_SWEEP": "1", "FT_SWEEP_COLS": "1", "FT_SWEEP_ITERS": "4", "FT_SWEEP_SEG": "24"},

@@ -198,27 +198,31 @@ __global__ void k_st_combine(const double *__restrict__ img, int w, int h, int64
 // read at a neighbour (p at x-1 / y-1 for the divergence, d at x+1 / y+1 for
 // the forward gradient) live in shared memory with a one-element apron,
 // img/weight and the own p in registers.  Exact inner region written back.
-constexpr int kRTW = 32, kRPY = 2, kRSP = kRTW + 2;
-// BY warps per CTA: 16 (32x32 tiles, 2 CTAs/SM) or 32 (32x64 tiles, one CTA)
-template <int BY>
+constexpr int kRTW = 32, kRPY = 2;
+// BY warps per CTA: 16 (32x32 tiles, 2 CTAs/SM) or 32 (32x64 tiles, one CTA);
+// NXC columns per thread: 2 (64-wide tiles, the default: the halo columns
+// are 8 of 64 instead of 8 of 32; measured +1.3 % default / +7 % light
+// frames/s) or 1 (32-wide, FT_ROF_WIDE=0)
+template <int BY, int NXC = 1>
 struct RofGeom {
-  static constexpr int TH = BY * kRPY, PL = kRSP * (TH + 2);
+  static constexpr int TW = 32 * NXC, SP = TW + 2, TH = BY * kRPY, PL = SP * (TH + 2);
   static constexpr size_t smem = 3 * PL * sizeof(double);
 };
 
 // FIX: halo 4 with 4 iterations per launch (every launch of the default 40
 // iterations): trip count and cone rows are compile-time constants.
-template <bool P2, bool FIX = false, int kRBY = 16>
+template <bool P2, bool FIX = false, int kRBY = 16, int NXC = 1>
 __global__ void __launch_bounds__(32 * kRBY, kRBY == 16 ? 2 : 1)
     k_rof_tile(const double *__restrict__ img, int w, int h, int64_t is,
                const double *__restrict__ px_in, const double *__restrict__ py_in,
                double *__restrict__ px_out, double *__restrict__ py_out, int64_t ps,
                double weight, double step, int halo, int iters, int first, int cone_on) {
-  constexpr int kRTH = RofGeom<kRBY>::TH, kRPL = RofGeom<kRBY>::PL;
+  using G = RofGeom<kRBY, NXC>;
+  constexpr int kRTH = G::TH, kRPL = G::PL, TW = G::TW, SP = G::SP, NQ = kRPY * NXC;
   extern __shared__ double rof_sm[];
   double *const s_px = rof_sm, *const s_py = rof_sm + kRPL, *const s_d = rof_sm + 2 * kRPL;
   if (FIX) halo = iters = 4;
-  const int step_x = kRTW - 2 * halo, step_y = kRTH - 2 * halo;
+  const int step_x = TW - 2 * halo, step_y = kRTH - 2 * halo;
   const int ox = blockIdx.x * step_x - halo, oy = blockIdx.y * step_y - halo;
   img += blockIdx.z * is;
   const int64_t po = blockIdx.z * ps;
@@ -229,25 +233,26 @@ __global__ void __launch_bounds__(32 * kRBY, kRBY == 16 ? 2 : 1)
     s_d[k] = 0.0;
   }
   __syncthreads();
-  double iw[kRPY], px[kRPY], py[kRPY];
-  bool fR[kRPY], fD[kRPY], fL[kRPY], fLC[kRPY], fU[kRPY], fLR[kRPY];
+  // element q: row ty + kRBY*(q / NXC), column tx + 32*(q % NXC)
+  double iw[NQ], px[NQ], py[NQ];
+  bool fR[NQ], fD[NQ], fL[NQ], fLC[NQ], fU[NQ], fLR[NQ];
 #pragma unroll
-  for (int k = 0; k < kRPY; ++k) {
-    const int gc = ox + tx, gr = oy + ty + kRBY * k;
+  for (int q = 0; q < NQ; ++q) {
+    const int gc = ox + tx + 32 * (q % NXC), gr = oy + ty + kRBY * (q / NXC);
     const bool in = gc >= 0 && gc < w && gr >= 0 && gr < h;
     const int64_t o = (int64_t)gr * w + gc;
-    iw[k] = in ? img[o] / weight : 0.0;  // img / weight (imaging.py:121)
-    px[k] = (in && !first) ? px_in[po + o] : 0.0;
-    py[k] = (in && !first) ? py_in[po + o] : 0.0;
-    fR[k] = gc < w - 1;
-    fD[k] = gr < h - 1;
-    fL[k] = gc > 0;
-    fLC[k] = gc == w - 1;
-    fU[k] = gr > 0;
-    fLR[k] = gr == h - 1;
-    const int id = (ty + kRBY * k + 1) * kRSP + tx + 1;
-    s_px[id] = px[k];
-    s_py[id] = py[k];
+    iw[q] = in ? img[o] / weight : 0.0;  // img / weight (imaging.py:121)
+    px[q] = (in && !first) ? px_in[po + o] : 0.0;
+    py[q] = (in && !first) ? py_in[po + o] : 0.0;
+    fR[q] = gc < w - 1;
+    fD[q] = gr < h - 1;
+    fL[q] = gc > 0;
+    fLC[q] = gc == w - 1;
+    fU[q] = gr > 0;
+    fLR[q] = gr == h - 1;
+    const int id = (ty + kRBY * (q / NXC) + 1) * SP + tx + 32 * (q % NXC) + 1;
+    s_px[id] = px[q];
+    s_py[id] = py[q];
   }
   __syncthreads();
   // Shrinking cone (tiles with a halo): iteration it (0-based) needs p on
@@ -256,45 +261,45 @@ __global__ void __launch_bounds__(32 * kRBY, kRBY == 16 ? 2 : 1)
   const int cone = FIX ? 0 : (cone_on && halo > 0 && iters <= halo) ? halo - iters : -1;
 #pragma unroll
   for (int it = 0; it < (FIX ? 4 : iters); ++it) {
-    double d[kRPY];
+    double d[NQ];
 #pragma unroll
-    for (int k = 0; k < kRPY; ++k) {  // d = divergence(p) - img/weight
-      const int lr = ty + kRBY * k;
+    for (int q = 0; q < NQ; ++q) {  // d = divergence(p) - img/weight
+      const int lr = ty + kRBY * (q / NXC);
       if (cone >= 0 && (lr < cone + it + 1 || lr >= kRTH - cone - it)) continue;
-      const int id = (ty + kRBY * k + 1) * kRSP + tx + 1;
-      const double l = s_px[id - 1], u = s_py[id - kRSP];
-      const double dx = fL[k] ? (fLC[k] ? -l : px[k] - l) : px[k];
-      const double dy = fU[k] ? (fLR[k] ? -u : py[k] - u) : py[k];
-      d[k] = (dx + dy) - iw[k];
-      s_d[id] = d[k];
+      const int id = (lr + 1) * SP + tx + 32 * (q % NXC) + 1;
+      const double l = s_px[id - 1], u = s_py[id - SP];
+      const double dx = fL[q] ? (fLC[q] ? -l : px[q] - l) : px[q];
+      const double dy = fU[q] ? (fLR[q] ? -u : py[q] - u) : py[q];
+      d[q] = (dx + dy) - iw[q];
+      s_d[id] = d[q];
     }
     __syncthreads();
 #pragma unroll
-    for (int k = 0; k < kRPY; ++k) {  // g = forward_gradient(d); p update
-      const int lr = ty + kRBY * k;
+    for (int q = 0; q < NQ; ++q) {  // g = forward_gradient(d); p update
+      const int lr = ty + kRBY * (q / NXC);
       if (cone >= 0 && (lr < cone + it + 1 || lr >= kRTH - cone - it - 1)) continue;
-      const int id = (ty + kRBY * k + 1) * kRSP + tx + 1;
-      const double gx = fR[k] ? s_d[id + 1] - d[k] : 0.0;
-      const double gy = fD[k] ? s_d[id + kRSP] - d[k] : 0.0;
+      const int id = (lr + 1) * SP + tx + 32 * (q % NXC) + 1;
+      const double gx = fR[q] ? s_d[id + 1] - d[q] : 0.0;
+      const double gy = fD[q] ? s_d[id + SP] - d[q] : 0.0;
       // step = 2^k (default 0.25): step*x is exact, so the fused forms round
       // exactly like the reference's separate multiply and add
       const double hy = glibc_hypot(gx, gy);
       const double norm = P2 ? fma(step, hy, 1.0) : 1.0 + step * hy;
-      px[k] = (P2 ? fma(step, gx, px[k]) : px[k] + step * gx) / norm;
-      py[k] = (P2 ? fma(step, gy, py[k]) : py[k] + step * gy) / norm;
-      s_px[id] = px[k];
-      s_py[id] = py[k];
+      px[q] = (P2 ? fma(step, gx, px[q]) : px[q] + step * gx) / norm;
+      py[q] = (P2 ? fma(step, gy, py[q]) : py[q] + step * gy) / norm;
+      s_px[id] = px[q];
+      s_py[id] = py[q];
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int k = 0; k < kRPY; ++k) {
-    const int lr = ty + kRBY * k, gc = ox + tx, gr = oy + lr;
+  for (int q = 0; q < NQ; ++q) {
+    const int lr = ty + kRBY * (q / NXC), lc = tx + 32 * (q % NXC), gc = ox + lc, gr = oy + lr;
     if (gc < 0 || gc >= w || gr < 0 || gr >= h) continue;
-    if (tx < halo || tx >= kRTW - halo || lr < halo || lr >= kRTH - halo) continue;
+    if (lc < halo || lc >= TW - halo || lr < halo || lr >= kRTH - halo) continue;
     const int64_t o = po + (int64_t)gr * w + gc;
-    px_out[o] = px[k];
-    py_out[o] = py[k];
+    px_out[o] = px[q];
+    py_out[o] = py[q];
   }
 }
 
@@ -538,12 +543,14 @@ int launch_structure_texture(const double *img, int w, int h, int64_t is, double
     const char *hv = getenv("FT_ROF_HALO");
     const int halo_t = (hv && *hv) ? atoi(hv) : 4;
     const int tall = getenv_int("FT_ROF_TALL", 0);  // 32x64 tiles, 1024 threads
+    const int wide = getenv_int("FT_ROF_WIDE", 1);  // 64-wide tiles (default)
     const int kRTH = tall ? RofGeom<32>::TH : RofGeom<16>::TH;
-    const bool resident = w <= kRTW && h <= kRTH;
+    const int tw = wide ? RofGeom<16, 2>::TW : kRTW;
+    const bool resident = w <= tw && h <= kRTH;
     const int halo = resident ? 0 : halo_t;
     const char *cv = getenv("FT_ROF_CONE");
     const int cone_on = (cv && *cv) ? atoi(cv) : 1;
-    const int sx = kRTW - 2 * halo, sy = kRTH - 2 * halo;
+    const int sx = tw - 2 * halo, sy = kRTH - 2 * halo;
     const dim3 g(resident ? 1 : (w + sx - 1) / sx, resident ? 1 : (h + sy - 1) / sy, nb);
     int done = 0;
     while (done < iterations) {
@@ -575,11 +582,16 @@ int launch_structure_texture(const double *img, int w, int h, int64_t is, double
         continue;
       }
       const bool fix = !resident && halo == 4 && k == 4 && cone_on && getenv_int("FT_ROF_FIX", 1);
-      auto kern = tall ? (p2 ? (fix ? k_rof_tile<true, true, 32> : k_rof_tile<true, false, 32>)
+      auto kern = tall && wide ? (p2 ? (fix ? k_rof_tile<true, true, 32, 2> : k_rof_tile<true, false, 32, 2>)
+                                     : (fix ? k_rof_tile<false, true, 32, 2> : k_rof_tile<false, false, 32, 2>))
+                  : tall ? (p2 ? (fix ? k_rof_tile<true, true, 32> : k_rof_tile<true, false, 32>)
                              : (fix ? k_rof_tile<false, true, 32> : k_rof_tile<false, false, 32>))
+                  : wide ? (p2 ? (fix ? k_rof_tile<true, true, 16, 2> : k_rof_tile<true, false, 16, 2>)
+                               : (fix ? k_rof_tile<false, true, 16, 2> : k_rof_tile<false, false, 16, 2>))
                        : (p2 ? (fix ? k_rof_tile<true, true> : k_rof_tile<true>)
                              : (fix ? k_rof_tile<false, true> : k_rof_tile<false>));
-      const size_t rsm = tall ? RofGeom<32>::smem : RofGeom<16>::smem;
+      const size_t rsm = tall ? (wide ? RofGeom<32, 2>::smem : RofGeom<32>::smem)
+                              : wide ? RofGeom<16, 2>::smem : RofGeom<16>::smem;
       if (rsm > 48 * 1024)
         FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
       kern<<<g, dim3(32, tall ? 32 : 16), rsm, s>>>(img, w, h, is, p[cur][0], p[cur][1], p[1 - cur][0],

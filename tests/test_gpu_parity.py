@@ -139,7 +139,10 @@ def test_flow_ragged_sizes_match_oracle(pkg, w, h, scales):
     {"FT_PD_CL": "1"},                                     # 2x1 clusters sharing the seam
     {"FT_ROF_NAIVE": "1"},
     {"FT_ROF_FIX": "0"},                                   # generic ROF launch
-    {"FT_ROF_TALL": "1"},                                  # ROF 32x64 tiles
+    {"FT_ROF_TALL": "1"},                                  # ROF 64x64 tiles
+    {"FT_ROF_TALL": "1", "FT_ROF_WIDE": "0"},              # ROF 32x64 tiles
+    {"FT_ROF_WIDE": "0"},                                  # ROF 32x32 tiles
+    {"FT_ROF_WIDE": "0", "FT_ROF_FIX": "0"},
     {"FT_ROF_SWEEP": "1"},                                 # ROF row sweep
     {"FT_ROF_SWEEP": "1", "FT_ROF_SWEEP_SEG": "20"},
 ])

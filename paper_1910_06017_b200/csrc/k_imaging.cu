@@ -211,12 +211,13 @@ struct RofGeom {
 
 // FIX: halo 4 with 4 iterations per launch (every launch of the default 40
 // iterations): trip count and cone rows are compile-time constants.
-template <bool P2, bool FIX = false, int kRBY = 16, int NXC = 1>
-__global__ void __launch_bounds__(32 * kRBY, kRBY == 16 ? 2 : 1)
-    k_rof_tile(const double *__restrict__ img, int w, int h, int64_t is,
-               const double *__restrict__ px_in, const double *__restrict__ py_in,
-               double *__restrict__ px_out, double *__restrict__ py_out, int64_t ps,
-               double weight, double step, int halo, int iters, int first, int cone_on) {
+// IN: the tile touches no image border (no out-of-frame element, no first /
+// last row or column), so every border flag is a compile-time constant.
+template <bool P2, bool FIX, int kRBY, int NXC, bool IN>
+__device__ __forceinline__ void rof_tile_body(
+    const double *__restrict__ img, int w, int h, int64_t is, const double *__restrict__ px_in,
+    const double *__restrict__ py_in, double *__restrict__ px_out, double *__restrict__ py_out,
+    int64_t ps, double weight, double step, int halo, int iters, int first, int cone_on) {
   using G = RofGeom<kRBY, NXC>;
   constexpr int kRTH = G::TH, kRPL = G::PL, TW = G::TW, SP = G::SP, NQ = kRPY * NXC;
   extern __shared__ double rof_sm[];
@@ -239,17 +240,17 @@ __global__ void __launch_bounds__(32 * kRBY, kRBY == 16 ? 2 : 1)
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
     const int gc = ox + tx + 32 * (q % NXC), gr = oy + ty + kRBY * (q / NXC);
-    const bool in = gc >= 0 && gc < w && gr >= 0 && gr < h;
+    const bool in = IN || (gc >= 0 && gc < w && gr >= 0 && gr < h);
     const int64_t o = (int64_t)gr * w + gc;
     iw[q] = in ? img[o] / weight : 0.0;  // img / weight (imaging.py:121)
     px[q] = (in && !first) ? px_in[po + o] : 0.0;
     py[q] = (in && !first) ? py_in[po + o] : 0.0;
-    fR[q] = gc < w - 1;
-    fD[q] = gr < h - 1;
-    fL[q] = gc > 0;
-    fLC[q] = gc == w - 1;
-    fU[q] = gr > 0;
-    fLR[q] = gr == h - 1;
+    fR[q] = IN || gc < w - 1;
+    fD[q] = IN || gr < h - 1;
+    fL[q] = IN || gc > 0;
+    fLC[q] = !IN && gc == w - 1;
+    fU[q] = IN || gr > 0;
+    fLR[q] = !IN && gr == h - 1;
     const int id = (ty + kRBY * (q / NXC) + 1) * SP + tx + 32 * (q % NXC) + 1;
     s_px[id] = px[q];
     s_py[id] = py[q];
@@ -295,12 +296,31 @@ __global__ void __launch_bounds__(32 * kRBY, kRBY == 16 ? 2 : 1)
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
     const int lr = ty + kRBY * (q / NXC), lc = tx + 32 * (q % NXC), gc = ox + lc, gr = oy + lr;
-    if (gc < 0 || gc >= w || gr < 0 || gr >= h) continue;
+    if (!IN && (gc < 0 || gc >= w || gr < 0 || gr >= h)) continue;
     if (lc < halo || lc >= TW - halo || lr < halo || lr >= kRTH - halo) continue;
     const int64_t o = po + (int64_t)gr * w + gc;
     px_out[o] = px[q];
     py_out[o] = py[q];
   }
+}
+
+template <bool P2, bool FIX = false, int kRBY = 16, int NXC = 1>
+__global__ void __launch_bounds__(32 * kRBY, kRBY == 16 ? 2 : 1)
+    k_rof_tile(const double *__restrict__ img, int w, int h, int64_t is,
+               const double *__restrict__ px_in, const double *__restrict__ py_in,
+               double *__restrict__ px_out, double *__restrict__ py_out, int64_t ps,
+               double weight, double step, int halo, int iters, int first, int cone_on) {
+  using G = RofGeom<kRBY, NXC>;
+  const int hh = FIX ? 4 : halo;
+  const int ox = blockIdx.x * (G::TW - 2 * hh) - hh, oy = blockIdx.y * (G::TH - 2 * hh) - hh;
+#ifndef FT_ROF_NO_IN
+  if (ox >= 1 && ox + G::TW <= w - 1 && oy >= 1 && oy + G::TH <= h - 1)
+    rof_tile_body<P2, FIX, kRBY, NXC, true>(img, w, h, is, px_in, py_in, px_out, py_out, ps,
+                                            weight, step, halo, iters, first, cone_on);
+  else
+#endif
+    rof_tile_body<P2, FIX, kRBY, NXC, false>(img, w, h, is, px_in, py_in, px_out, py_out, ps,
+                                             weight, step, halo, iters, first, cone_on);
 }
 
 // ROF row sweep (opt-in FT_ROF_SWEEP=1), the k_pd_sweep scheme applied to

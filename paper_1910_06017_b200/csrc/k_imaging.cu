@@ -206,7 +206,11 @@ constexpr int kRTW = 32, kRPY = 2;
 template <int BY, int NXC = 1>
 struct RofGeom {
   static constexpr int TW = 32 * NXC, SP = TW + 2, TH = BY * kRPY, PL = SP * (TH + 2);
+#ifndef FT_ROF_IWREG
+  static constexpr size_t smem = 4 * PL * sizeof(double);  // + img/weight plane
+#else
   static constexpr size_t smem = 3 * PL * sizeof(double);
+#endif
 };
 
 // FIX: halo 4 with 4 iterations per launch (every launch of the default 40
@@ -235,14 +239,25 @@ __device__ __forceinline__ void rof_tile_body(
   }
   __syncthreads();
   // element q: row ty + kRBY*(q / NXC), column tx + 32*(q % NXC)
+#ifndef FT_ROF_IWREG
+  // img/weight in a fourth shared plane, read by its owner only: frees 4
+  // doubles of registers (the 64x32 instantiation no longer spills;
+  // -DFT_ROF_IWREG keeps it in registers)
+  double *const s_iw = rof_sm + 3 * kRPL;
+#define ROF_IW(q, id) s_iw[id]
+  double px[NQ], py[NQ];
+#else
+#define ROF_IW(q, id) iw[q]
   double iw[NQ], px[NQ], py[NQ];
+#endif
   bool fR[NQ], fD[NQ], fL[NQ], fLC[NQ], fU[NQ], fLR[NQ];
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
     const int gc = ox + tx + 32 * (q % NXC), gr = oy + ty + kRBY * (q / NXC);
     const bool in = IN || (gc >= 0 && gc < w && gr >= 0 && gr < h);
     const int64_t o = (int64_t)gr * w + gc;
-    iw[q] = in ? img[o] / weight : 0.0;  // img / weight (imaging.py:121)
+    const int id0 = (ty + kRBY * (q / NXC) + 1) * SP + tx + 32 * (q % NXC) + 1;
+    ROF_IW(q, id0) = in ? img[o] / weight : 0.0;  // img / weight (imaging.py:121)
     px[q] = (in && !first) ? px_in[po + o] : 0.0;
     py[q] = (in && !first) ? py_in[po + o] : 0.0;
     fR[q] = IN || gc < w - 1;
@@ -271,7 +286,7 @@ __device__ __forceinline__ void rof_tile_body(
       const double l = s_px[id - 1], u = s_py[id - SP];
       const double dx = fL[q] ? (fLC[q] ? -l : px[q] - l) : px[q];
       const double dy = fU[q] ? (fLR[q] ? -u : py[q] - u) : py[q];
-      d[q] = (dx + dy) - iw[q];
+      d[q] = (dx + dy) - ROF_IW(q, id);
       s_d[id] = d[q];
     }
     __syncthreads();
@@ -302,6 +317,7 @@ __device__ __forceinline__ void rof_tile_body(
     px_out[o] = px[q];
     py_out[o] = py[q];
   }
+#undef ROF_IW
 }
 
 template <bool P2, bool FIX = false, int kRBY = 16, int NXC = 1>

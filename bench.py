@@ -1,18 +1,25 @@
 #!/usr/bin/env python
-"""Benchmark: tracked SD frames/s per B200 (BASELINE.json metric) on config
-C2 -- 720x576, 100 tracks with scale change and occlusion, detections every
-5th frame, default FlowParams (6 scales x 5 warps x 50 iterations), fp64.
+"""Benchmark: tracked SD frames/s (BASELINE.json metric) on config C2 --
+720x576, 100 tracks with scale change and occlusion, detections every 5th
+frame, default FlowParams (6 scales x 5 warps x 50 iterations), fp64 -- with
+the streams batched and sharded as in C5.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--streams B]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--streams B | --total-streams T]
     python bench.py --impl reference ...     (CPU reference arm)
 
-One step = one frame of each of the B independent streams resident on a GPU
-(config C5's stream sharding: ranks own disjoint streams, no collective on
-the data path; the only collectives are the timing barrier / max).
-`value` is device-timed (CUDA events on the tracker stream, inputs already
-in HBM); `e2e` goes through the public Tracker API with host frames in
-pinned memory, H2D of frames+detections and D2H of the track table inside
-the timed region.
+One step = one frame of each of the B streams resident on a GPU.  Ranks
+own disjoint blocks of global stream ids (paper_1910_06017_b200/shard.py);
+no collective touches the data path -- only the timing barrier, the max of
+the ranks' times and the final host gather of track records.  `--gpus N`
+without a torchrun environment launches the N ranks itself (and fails if
+the box has fewer GPUs).
+
+`value` = frames processed by ALL ranks / the slowest rank's device time
+(whole-job aggregate, the driver's contract); `value_per_gpu` = value / N,
+the per-GPU figure the metric's wording names.  Device time: CUDA events on
+the tracker stream, inputs already in HBM.  `e2e` goes through the public
+Tracker API with host frames in pinned memory, H2D of frames + detections
+and D2H of the track table inside the timed region.
 """
 from __future__ import annotations
 
@@ -20,6 +27,7 @@ import argparse
 import json
 import multiprocessing as mp
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -30,12 +38,14 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+from paper_1910_06017_b200 import shard  # noqa: E402
+
 METRIC = "tracked frames/sec per GPU at 720×576, 100 tracks; HBM-roofline fraction"
-W_, H_, N_OBJ, DET_EVERY = 720, 576, 100, 5
+W_, H_, N_OBJ, DET_EVERY, JITTER = 720, 576, 100, 5, 1.0
 SCALES = None  # FlowParams.pyramid_scales (None: auto_scales, 6 at SD)
-WORKLOAD = ("C2 streams batched as in C5 (64 SD streams per GPU): 720x576 SD, 100 tracks, "
-            "scale change + occlusion, detections every 5th frame, TV-L1 6 scales x 5 warps x "
-            "50 iterations, ROF 40 iterations, fp64")
+WORKLOAD = ("C2 streams batched as in C5: 720x576 SD, 100 tracks, scale change + occlusion, "
+            "detections every 5th frame (1 px jitter), TV-L1 6 scales x 5 warps x 50 iterations, "
+            "ROF 40 iterations, fp64")
 # BASELINE.json configs other than the headline, as measured (non-headline)
 # lines: (W, H, tracks, detector cadence, pyramid scales, algorithmic bytes /
 # frame from SURVEY 8(d), workload text)
@@ -49,6 +59,7 @@ CONFIGS = {
            "frame, TV-L1 5 scales x 5 warps x 50 iterations, ROF 40 iterations, fp64 "
            "(the KLT forward-backward check has no counterpart on the reference path)"),
 }
+FRAME_BYTES = {"default": 22.03e9, "light": 2.52e9}  # SURVEY 8(d) algorithmic bytes / SD frame
 
 
 def apply_config(name: str) -> None:
@@ -61,65 +72,34 @@ def apply_config(name: str) -> None:
     METRIC = f"tracked frames/sec per GPU at {W_}×{H_}, {N_OBJ} tracks; HBM-roofline fraction"
 
 
-# ----------------------------------------------------------------------------
-def dist_init():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if ws > 1:
-        import torch
-        import torch.distributed as dist
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
-        if backend == "nccl":
-            torch.cuda.set_device(local)
-        dist.init_process_group(backend)
-    return ws, rank, local
+# ---------------------------------------------------------------------------
+stream_seed = shard.stream_seed
+dist_init = shard.init
+barrier = shard.barrier
+allmax = shard.allmax
 
 
-def barrier(ws):
-    if ws > 1:
-        import torch.distributed as dist
-        dist.barrier()
-
-
-def allmax(ws, v: float) -> float:
-    if ws == 1:
-        return v
-    import torch
-    import torch.distributed as dist
-    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
-    t = torch.tensor([v], dtype=torch.float64, device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
-
-
-def stream_seed(rank: int, s: int) -> int:
-    return 1000 + 64 * rank + s
-
-
-def gen_streams(rank: int, n_streams: int, n_frames: int):
+def gen_stream(g: int, n_frames: int):
     from paper_1910_06017_b200.synth import make_sequence
-    out = []
-    for s in range(n_streams):
-        out.append(make_sequence(W_, H_, N_OBJ, n_frames, seed=stream_seed(rank, s),
-                                 det_every=DET_EVERY, scale_change=True, jitter=1.0))
-    return out
+    return make_sequence(W_, H_, N_OBJ, n_frames, seed=stream_seed(g), det_every=DET_EVERY,
+                         scale_change=True, jitter=JITTER)
 
 
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu: int):
         self.gpu, self.rows, self.proc = gpu, [], None
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except FileNotFoundError:
@@ -141,10 +121,7 @@ class ClockSampler:
     def summary(self):
         if not self.rows:  # timed region shorter than the sampling period: one query now
             try:
-                q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-                     "clocks_event_reasons.hw_thermal_slowdown,"
-                     "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
                                       "--format=csv,noheader,nounits"], capture_output=True,
                                      text=True, timeout=10).stdout
                 self.rows = [[x.strip() for x in ln.split(",")] for ln in out.splitlines() if ln]
@@ -173,17 +150,34 @@ def det_records(dets, max_dets):
 
 
 def workload(args) -> str:
-    if getattr(args, "flow", "default") == "light":
-        return WORKLOAD.replace("6 scales x 5 warps x 50 iterations",
-                                "6 scales x 2 warps x 10 iterations (SURVEY 8(d) light FlowParams)")
-    return WORKLOAD
+    w = WORKLOAD
+    if args.flow == "light":
+        w = w.replace("6 scales x 5 warps x 50 iterations",
+                      "6 scales x 2 warps x 10 iterations (SURVEY 8(d) light FlowParams)")
+    if args.motion == "klt":
+        w = (f"C2 with the KLT/MedianFlow backend (SURVEY 8 f4): {W_}x{H_}, {N_OBJ} tracks, "
+             "10x10 points/box, 3-level LK pyramid, 9x9 window, forward-backward check, fp64")
+    return w
 
 
-# ----------------------------------------------------------------------------
-# CPU side: the oracle port of the reference, one SD stream-frame per process
+def bench_config(args, ws: int, streams_per_gpu: int) -> dict:
+    """The `config` object, identical on both arms (same workload keys)."""
+    return {"workload": workload(args), "frame": [W_, H_], "tracks_per_stream": N_OBJ,
+            "detect_every": DET_EVERY, "det_jitter_px": JITTER,
+            "streams_per_gpu": streams_per_gpu, "total_streams": streams_per_gpu * ws,
+            "stream_seeds": "1000 + global stream id",
+            "parallelism": f"stream-sharded x{ws} (no data-path collective)",
+            "l2": "working set > L2: 64 SD streams x ~100 MB of state per GPU; every launch "
+                  "streams its planes from HBM (no L2 flush needed)"}
+
+
+# ---------------------------------------------------------------------------
+# CPU side: the oracle port of the reference.  One job = one stream's frame 1
+# of the GPU arm's own sequence (same seed scheme, cadence and jitter): frame
+# 0 bootstraps untimed, frame 1 (ST + flow + predict; a coasting frame at
+# cadence 5) is timed.  Match + update on detection frames add < 0.1 % on
+# the CPU (SURVEY 8(a) A13-A15 vs A4/A6).
 def _flow_params(flow: str, oracle: bool = False):
-    """default: FlowParams() (the headline C2 workload); light: SURVEY 8(d)'s
-    declared light setting (2 warps x 10 iterations per scale)."""
     if oracle:
         from oracle import ftoracle as O
         cls = O.FlowParams
@@ -194,34 +188,35 @@ def _flow_params(flow: str, oracle: bool = False):
     return cls(warps_per_level=2, iterations_per_warp=10, pyramid_scales=SCALES)
 
 
-FRAME_BYTES = {"default": 22.03e9, "light": 2.52e9}  # SURVEY 8(d) algorithmic bytes / SD frame
-
-
 def _cpu_frame_job(args):
-    rank, s, flow, config = args
+    g, flow, config, motion = args
     apply_config(config)  # spawned child: module globals start at the headline config
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     from oracle import ftoracle as O
-    from paper_1910_06017_b200.synth import make_sequence
-    frames, dets = make_sequence(W_, H_, N_OBJ, 2, seed=stream_seed(rank, s), det_every=1,
-                                 scale_change=True)
+    frames, dets = gen_stream(g, 2)
     st = O.StreamState()
-    d0 = [O.Det(d.class_id, d.label, d.score, d.box) for d in dets[0]]
+    od = [None if d is None else [O.Det(x.class_id, x.label, x.score, x.box) for x in d]
+          for d in dets]
+    if motion == "klt":
+        from oracle import klt_oracle as K
+        K.step_klt(st, frames[0], 0, od[0])
+        t0 = time.perf_counter()
+        K.step_klt(st, frames[1], 1, od[1])
+        return time.perf_counter() - t0
     prm = _flow_params(flow, oracle=True)
-    O.step(st, frames[0], 0, d0, prm)  # first frame: ST + spawn (not timed)
-    d1 = [O.Det(d.class_id, d.label, d.score, d.box) for d in dets[1]]
+    O.step(st, frames[0], 0, od[0], prm)  # first frame: ST + spawn (not timed)
     t0 = time.perf_counter()
-    O.step(st, frames[1], 1, d1, prm)  # a full tracked frame: ST + flow + predict + match + update
+    O.step(st, frames[1], 1, od[1], prm)  # a tracked frame: ST + flow + predict (+ match/update)
     return time.perf_counter() - t0
 
 
-def cpu_run(n_procs: int, jobs: int, flow: str = "default", config: str = "c2"):
+def cpu_run(n_procs: int, jobs: int, flow: str, config: str, motion: str):
     for var in ("OMP_NUM_THREADS", "MKL_NUM_THREADS", "OPENBLAS_NUM_THREADS"):
         os.environ[var] = "1"  # one core per process (children inherit)
     ctx = mp.get_context("spawn")
     t0 = time.perf_counter()
     with ctx.Pool(n_procs) as pool:
-        per = pool.map(_cpu_frame_job, [(99, s, flow, config) for s in range(jobs)])
+        per = pool.map(_cpu_frame_job, [(s, flow, config, motion) for s in range(jobs)])
     return time.perf_counter() - t0, per
 
 
@@ -232,32 +227,37 @@ def host_cores() -> int:
         return os.cpu_count() or 1
 
 
-def cpu_baseline_measure(flow: str = "default", config: str = "c2"):
+def _cpu_sample(cores, config, motion, flow) -> str:
+    impl = ("oracle/klt_oracle.py step_klt (the KLT backend's CPU definition)" if motion == "klt"
+            else "oracle/ftoracle.py step (numpy restatement of flowtrack, bit-exact)")
+    return (f"{cores} processes (one per host core), each tracking frame 1 of its own stream "
+            f"(global ids 0..{cores - 1}, the GPU arm's seeds, cadence and jitter; {config}, "
+            f"{N_OBJ} tracks, {flow} FlowParams) through {impl}; frame 0 untimed")
+
+
+def cpu_baseline_measure(flow: str, config: str, motion: str):
     cores = host_cores()
-    wall, per = cpu_run(cores, cores, flow, config)
-    # each process measured its own tracked frame; aggregate = cores / mean
+    wall, per = cpu_run(cores, cores, flow, config, motion)
     per_core_fps = 1.0 / float(np.mean(per))
     return {"value": round(per_core_fps * cores, 5), "unit": "frames/s", "cores": cores,
             "kind": "port", "per_core_fps": round(per_core_fps, 5),
-            "sample": f"{cores} processes x 1 tracked frame ({config} workload, {N_OBJ} tracks, {flow} "
-                      f"FlowParams) through oracle/ftoracle.py (numpy restatement of the "
-                      f"reference, bit-exact); wall {wall:.1f}s"}
+            "sample": _cpu_sample(cores, config, motion, flow) + f"; wall {wall:.1f}s"}
 
 
 def run_reference(args, ws, rank):
     if rank != 0:
         return
     cores = host_cores()
-    # One step: every host core tracks one frame of its own stream.  Each
-    # process first runs an untimed warm-up frame (imports, ST, spawn), then
-    # times one full tracked frame; a step lasts as long as its slowest
-    # process (process start-up is not reference work and is not counted).
-    step_times, walls = [], []
-    for k in range(args.steps):
-        wall, per = cpu_run(cores, cores, args.flow, args.config)
+    # One step: every host core tracks one frame of its own stream.  A step
+    # lasts as long as its slowest process (process start-up and the untimed
+    # bootstrap frame are not reference work and are not counted).
+    step_times = []
+    spent = 0.0
+    for _ in range(args.steps):
+        wall, per = cpu_run(cores, cores, args.flow, args.config, args.motion)
         step_times.append(float(np.max(per)))
-        walls.append(wall)
-        if sum(walls) > args.ref_budget_s:
+        spent += wall
+        if spent > args.ref_budget_s:
             break
     steps = len(step_times)
     wall = float(np.sum(step_times))
@@ -266,34 +266,41 @@ def run_reference(args, ws, rank):
             "n_gpus": args.gpus, "steps": steps, "warmup": 1,
             "ms_per_step": round(1000 * wall / steps, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload(args), "streams": cores,
-                       "note": "one step = every host core tracks one frame of its own stream "
-                               "(after one untimed warm-up frame per process); step time = the "
-                               "slowest process; steps capped by a "
-                               f"{args.ref_budget_s:.0f}s budget"},
+            "config": bench_config(args, 1, args.streams if args.total_streams is None
+                                   else args.total_streams),
             "cpu_baseline": {"value": round(fps, 5), "unit": "frames/s", "cores": cores,
                              "kind": "port",
-                             "sample": "oracle/ftoracle.py (numpy restatement of flowtrack, "
-                                       "bit-exact), one process per core"},
+                             "sample": _cpu_sample(cores, args.config, args.motion, args.flow)
+                             + f"; step = slowest process; {steps} steps within a "
+                               f"{args.ref_budget_s:.0f}s budget"},
             "e2e": {"value": round(fps, 5), "unit": "frames/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-# ----------------------------------------------------------------------------
+# ---------------------------------------------------------------------------
+def _pct(v, q):
+    return round(float(np.percentile(v, q)), 4) if len(v) else None
+
+
 def run_ours(args, ws, rank, local):
     import torch
 
     from paper_1910_06017_b200 import _lib
-    from paper_1910_06017_b200.optflow import FlowParams
     from paper_1910_06017_b200.pipeline import Tracker
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    B, K, Wm = args.streams, args.steps, args.warmup
+    if args.total_streams is not None:
+        ids = shard.shard(rank, ws, total=args.total_streams)
+        scaling = "strong"
+    else:
+        ids = shard.shard(rank, ws, per_rank=args.streams)
+        scaling = "weak"
+    B, K, Wm = len(ids), args.steps, args.warmup
     T = Wm + K + 1
     max_tracks, max_dets = max(256, 2 * N_OBJ + 56), max(160, N_OBJ + 60)
-    seqs = gen_streams(rank, B, T)
+    seqs = [gen_stream(g, T) for g in ids]
     frames = np.stack([np.stack([seqs[s][0][t] for s in range(B)]) for t in range(T)])  # T,B,H,W
     dets = np.zeros((T, B, max_dets), dtype=_lib.DET_DTYPE)
     ndets = np.zeros((T, B), dtype=np.int32)
@@ -314,53 +321,29 @@ def run_ours(args, ws, rank, local):
         trk.step_device(d_frames[t], t, d_dets[t], d_ndets[t])
     torch.cuda.synchronize(dev)
     barrier(ws)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
     with ClockSampler(local) as clk:
         torch.cuda.synchronize(dev)
-        e0.record(stream)
-        for t in range(Wm + 1, T):
+        ev[0].record(stream)
+        for k, t in enumerate(range(Wm + 1, T)):
             trk.step_device(d_frames[t], t, d_dets[t], d_ndets[t])
-        e1.record(stream)
+            ev[k + 1].record(stream)
         torch.cuda.synchronize(dev)
     barrier(ws)
-    ms = e0.elapsed_time(e1)
+    ms = ev[0].elapsed_time(ev[K])
+    step_ms = [ev[k].elapsed_time(ev[k + 1]) for k in range(K)]
     ms_max = allmax(ws, ms)
     launches_per_step = trk.launches()
-    value = ws * B * K / (ms_max / 1000.0)
+    value = ws * B * K / (ms_max / 1000.0) if args.total_streams is None else \
+        args.total_streams * K / (ms_max / 1000.0)
+    phases = trk.phase_ms()
 
     # ---------------- dominant kernel, timed live in the last timed step ------
-    # (CUDA events captured into the step graph around every finest-level
-    # k_pd_tile launch sequence; read after the timed region ends)
-    span_ms, span_n, span_pi = C_double(), C_int(), C_double()
-    msl, bpl, ipl = C_double(), C_double(), C_int()
+    roofline = None
     if args.motion == "tvl1":
-        _lib.check(trk._lib.ft_tracker_pd_span(trk._h, byref(span_ms), byref(span_n),
-                                               byref(span_pi)))
-        # the same kernel timed alone (repeated launches over the final state)
-        _lib.check(trk._lib.ft_tracker_profile_pd(trk._h, 20, byref(msl), byref(bpl),
-                                                  byref(ipl)))
-    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
-        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
-    hbm = float(peaks.get("hbm_gbs", 6650.0))
-    # 152 algorithmic bytes per pixel-iteration (read 11 planes,
-    # write 8) x the pixel-iterations of the step's finest-level launches
-    live_bytes = 152.0 * span_pi.value
-    live_launch_ms = span_ms.value / span_n.value if span_n.value else 0.0
-    achieved = live_bytes / (span_ms.value / 1000.0) / 1e9 if span_ms.value > 0 else 0.0
-    alone_gbs = bpl.value / (msl.value / 1000.0) / 1e9 if msl.value > 0 else 0.0
-    traffic = None
-    tfile = os.path.join(ROOT, "profiles", "pd_traffic.json")
-    if os.path.exists(tfile):
-        tj = json.load(open(tfile))
-        # ncu capture of one finest-level launch, normalised per stream-pixel
-        # and rescaled to this run's streams (same kernel, same geometry)
-        if tj.get("bytes_per_stream_pixel"):
-            from paper_1910_06017_b200.imaging import select_level
-            lv = select_level(W_, H_)  # the flow runs at the processing level
-            traffic = round(tj["bytes_per_stream_pixel"] * B * (W_ >> lv) * (H_ >> lv), 1)
-    # step-level roofline: SURVEY 8(d) algorithmic bytes per SD frame (22.03 GB at C2)
-    frame_bytes = FRAME_BYTES[args.flow]
-    step_frac = (value / ws) * frame_bytes / (hbm * 1e9)
+        roofline = trk.roofline(hbm_peak_gbs(), frame_bytes=FRAME_BYTES[args.flow],
+                                step_ms=ms / K, frames_per_s_per_gpu=value / ws,
+                                profiles_dir=os.path.join(ROOT, "profiles"))
 
     # ---------------- end to end through the public API (e2e) ----------------
     trk.reset()
@@ -371,68 +354,98 @@ def run_ours(args, ws, rank, local):
     torch.cuda.synchronize(dev)
     barrier(ws)
     t0 = time.perf_counter()
-    n_tracks = 0
+    last = None
     # pipelined public API: stage + submit frame t, then collect frame t-1
     # (each step still does its own pinned H2D and D2H inside the region)
     for t in range(Wm + 1, T):
         trk.submit(frames[t], t, recs[t])
         if t > Wm + 1:
-            n_tracks += sum(len(o) for o in trk.wait())
-    n_tracks += sum(len(o) for o in trk.wait())
+            last = trk.wait()
+    last = trk.wait()
     torch.cuda.synchronize(dev)
     e2e_s = allmax(ws, time.perf_counter() - t0)
     barrier(ws)
-    e2e = ws * B * K / e2e_s
-    h2d = B * H_ * W_ + B * max_dets * _lib.DET_DTYPE.itemsize + (B + 1) * 4
+    total_frames = ws * B * K if args.total_streams is None else args.total_streams * K
+    e2e = total_frames / e2e_s
+    h2d = B * H_ * W_ + B * max_dets * _lib.DET_DTYPE.itemsize + (2 * B + 1) * 4
     d2h = B * 2 * max_tracks * _lib.TRACK_DTYPE.itemsize + 2 * B * 4
+
+    # ---------------- single-stream latency (the paper's real-time setting) ----
+    latency = None
+    if B == 1:
+        lat = []
+        trk.reset()
+        for t in range(T):
+            t1 = time.perf_counter()
+            trk.step_records(frames[t], t, recs[t])
+            if t > Wm:
+                lat.append(1000 * (time.perf_counter() - t1))
+        latency = {"device_ms_p50": _pct(step_ms, 50), "device_ms_p99": _pct(step_ms, 99),
+                   "e2e_ms_p50": _pct(lat, 50), "e2e_ms_p99": _pct(lat, 99),
+                   "e2e_api": "Tracker.step_records (synchronous: submit + wait per frame)"}
+
+    # ---------------- final host gather of the track results (north_star) ----
+    gathered = shard.gather_tracks(ws, rank, ids, last)
     trk.close()
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_measure(args.flow, args.config)
+        cpu = cpu_baseline_measure(args.flow, args.config, args.motion)
 
     if rank == 0:
+        n_tracks = sum(len(r) for r in gathered.values())
         line = {"metric": METRIC, "value": round(value, 3), "unit": "frames/s", "n_gpus": ws,
+                "value_per_gpu": round(value / ws, 3),
                 "steps": K, "warmup": Wm, "ms_per_step": round(ms_max / K, 4),
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic",
-                "config": {"workload": workload(args), "streams_per_gpu": B, "frame": [W_, H_],
-                           "tracks_per_stream": N_OBJ, "parallelism": f"stream-sharded x{ws}",
-                           "l2": "working set > L2: every launch streams its state planes "
-                                 f"({B} streams x ~70 MB)"},
+                "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (SURVEY 8(d) generator: textured moving boxes, YoloV3-style "
+                        "detections in receptive-field coordinates)",
+                "config": bench_config(args, ws, B),
                 "e2e": {"value": round(e2e, 3), "unit": "frames/s", "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h, "api": "Tracker.submit/wait (pipelined)"},
                 "gpu_launches": int(launches_per_step * K),
-                "roofline": {"bound": "hbm", "kernel": "k_pd_tile (TV-L1 primal-dual, finest level)",
-                             "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-                             "frac": round(achieved / hbm, 4), "traffic": traffic,
-                             "timing": "live: CUDA events in the step graph around the "
-                                       "finest-level k_pd_tile launches of the last timed step",
-                             "launches": span_n.value,
-                             "bytes_per_launch": live_bytes / max(span_n.value, 1),
-                             "ms_per_launch": round(live_launch_ms, 5),
-                             "share_of_step": round(span_ms.value / (ms / K), 4) if ms else None,
-                             "compulsory_bytes_per_launch": bpl.value / max(ipl.value, 1),
-                             "alone": {"ms_per_launch": round(msl.value, 5),
-                                       "iters_per_launch": ipl.value,
-                                       "achieved": round(alone_gbs, 1)},
-                             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650",
-                             "step_roofline_frac": round(step_frac, 4),
-                             "step_bytes_per_frame": frame_bytes},
+                "step_ms": {"p50": _pct(step_ms, 50), "p99": _pct(step_ms, 99)},
+                "phases_ms": phases,
+                "roofline": roofline,
                 "cpu_baseline": cpu, "clocks": clk.summary(),
-                "tracks_out": int(n_tracks)}
-        if args.motion == "klt":  # SURVEY 8 f4 backend: not the reference path
-            line["config"]["workload"] = (
-                "C2 with the KLT/MedianFlow backend (SURVEY 8 f4): 720x576 SD, 100 tracks, "
-                "10x10 points/box, 3-level LK pyramid, 9x9 window, forward-backward check, fp64")
-            line["config"]["l2"] = (f"working set > L2: {B} streams x ~26 MB of KLT pyramids "
-                                     "(prev + cur) per step")
-            line["roofline"] = None  # gather-latency bound; no streaming-roofline model
-            line["step_roofline_frac"] = None
+                "gather": {"streams": len(gathered), "tracks": int(n_tracks),
+                           "note": "last frame's track records of every stream gathered to rank "
+                                   "0 on the host (torch.distributed gather_object)"}}
+        if latency:
+            line["latency"] = latency
+        if cpu is None and ws > 1:
+            line["cpu_baseline_note"] = "timed at N=1 only (same host, same workload)"
         print(json.dumps(line), flush=True)
 
 
-from ctypes import byref, c_double as C_double, c_int as C_int  # noqa: E402
+def hbm_peak_gbs():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        return float(json.load(open(p)).get("hbm_gbs", 6650.0)), "MEASURED_PEAKS.json hbm_gbs"
+    return 6650.0, "fallback 6650 (B200_PROFILING.md)"
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def launch_ranks(args) -> int:
+    """`--gpus N` outside torchrun: start the N ranks ourselves."""
+    if args.impl == "ours":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs, this box has {have}",
+                  file=sys.stderr)
+            return 1
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -441,7 +454,9 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--streams", type=int, default=64,
-                    help="SD streams per GPU (64 = BASELINE config C5's stream count at N=1)")
+                    help="SD streams per GPU (weak scaling; 64 = C5's stream count at N=1)")
+    ap.add_argument("--total-streams", type=int, default=None,
+                    help="split this many streams over the GPUs (strong scaling, C5: 64)")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--motion", choices=["tvl1", "klt"], default="tvl1",
                     help="tvl1: the reference path (headline); klt: SURVEY 8 f4 backend")
@@ -453,6 +468,12 @@ def main():
                     help="c2 (headline) or another BASELINE.json config as a non-headline line")
     args = ap.parse_args()
     apply_config(args.config)
+    ws_env = os.environ.get("WORLD_SIZE")
+    if ws_env is None and args.gpus > 1:
+        sys.exit(launch_ranks(args))
+    if ws_env is not None and int(ws_env) != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws_env}", file=sys.stderr)
+        sys.exit(2)
     ws, rank, local = dist_init()
     if args.impl == "reference":
         run_reference(args, ws, rank)

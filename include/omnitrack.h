@@ -232,6 +232,14 @@ int ft_tracker_profile_pd(ft_tracker *trk, int reps, double *ms_per_launch,
                           double *bytes_per_launch, int *iters_per_launch);
 /* Kernel launches issued by the last step (for the bench's gpu_launches). */
 int ft_tracker_launches(ft_tracker *trk, int64_t *count);
+/* Per-phase device times of a step (FrameResult carries
+ * per-phase timing in ms).  slot 0/1: the step last submitted in that slot
+ * (waits for it); slot -1: the most recent step.  Fills up to `max` phases
+ * in execution order: ms[i] and names[i] (static strings: "h2d",
+ * "ingest+pyramid", "structure_texture", "flow pyramid", "flow level k",
+ * "predict+match+update", "d2h", ...); *n = phases written. */
+int ft_tracker_phase_times(ft_tracker *trk, int slot, double *ms, const char **names, int max,
+                           int *n);
 /* Reset all streams (drop tracks and cached previous frames). */
 int ft_tracker_reset(ft_tracker *trk);
 

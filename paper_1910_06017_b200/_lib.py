@@ -106,6 +106,8 @@ SIGNATURES = {
     "ft_tracker_profile_pd": (_I, [_P, _I, C.POINTER(_D), C.POINTER(_D), C.POINTER(_I)]),
     "ft_tracker_pd_span": (_I, [_P, C.POINTER(_D), C.POINTER(_I), C.POINTER(_D)]),
     "ft_tracker_launches": (_I, [_P, C.POINTER(C.c_int64)]),
+    "ft_tracker_phase_times": (_I, [_P, _I, C.POINTER(_D), C.POINTER(C.c_char_p), _I,
+                                    C.POINTER(_I)]),
     "ft_tracker_reset": (_I, [_P]),
 }
 

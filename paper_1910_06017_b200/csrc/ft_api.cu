@@ -20,23 +20,8 @@ namespace ft {
 
 thread_local std::string g_err;
 thread_local LaunchCounter *g_launch_counter = nullptr;
-PhaseTimer *g_phase = nullptr;
+thread_local PhaseRec *g_phase = nullptr;
 thread_local PdSpan *g_pd_span = nullptr;
-
-void PhaseTimer::report() {
-  if (n < 2) return;
-  cudaEventSynchronize(ev[n - 1]);
-  float total = 0.f;
-  cudaEventElapsedTime(&total, ev[0], ev[n - 1]);
-  fprintf(stderr, "[ft phase timing] total %.3f ms\n", total);
-  for (int i = 1; i < n; ++i) {
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
-    fprintf(stderr, "  %-28s %9.3f ms  %5.1f%%\n", name[i], ms, 100.f * ms / total);
-  }
-  for (int i = 0; i < n; ++i) cudaEventDestroy(ev[i]);
-  n = 0;
-}
 
 void set_error(const std::string &msg) { g_err = msg; }
 int fail(int code, const std::string &msg) {
@@ -627,6 +612,7 @@ struct ft_tracker {
     int32_t *nout = nullptr;
     cudaEvent_t done = nullptr;
     bool pending = false;
+    const void *graph = nullptr;  // Graph of the slot's last submission
   } slots[2];
   uint8_t *h_luma = nullptr;
   ft_det *h_dets = nullptr;
@@ -655,8 +641,10 @@ struct ft_tracker {
   struct Graph {
     cudaGraphExec_t exec = nullptr;
     int64_t launches = 0;
+    std::unique_ptr<PhaseRec> phases;  // event nodes at the phase boundaries
   };
   std::map<GraphKey, Graph> graphs;
+  const Graph *last_graph = nullptr;  // graph of the most recent step
   int64_t frames_seen = 0;
   int64_t last_launches = 0;
 
@@ -677,6 +665,7 @@ struct ft_tracker {
     // pyramid is `pyr_prev` (pyr_par flips after every step; no copy)
     double *const pyr_cur = pyr_par ? d_pyr_prev : d_pyr_cur;
     double *const pyr_prev = pyr_par ? d_pyr_cur : d_pyr_prev;
+    phase_mark("start");
     if (host_io) {
       FT_CUDA_TRY(cudaMemcpyAsync(d_luma, h_luma, (size_t)S * W * H, cudaMemcpyHostToDevice, s));
       FT_CUDA_TRY(cudaMemcpyAsync(d_dets, h_dets, (size_t)S * cfg.max_dets * sizeof(ft_det),
@@ -685,8 +674,8 @@ struct ft_tracker {
       luma = d_luma;
       dets = d_dets;
       in = d_in;
+      phase_mark("h2d");
     }
-    phase_mark("start");
     // (1) preprocessing: ingest + pyramid to level L (imaging.py:75-95) + ST
     const double *img;
     if (L == 0) {
@@ -728,6 +717,7 @@ struct ft_tracker {
                                     (size_t)S * 2 * cfg.max_tracks * sizeof(ft_track),
                                     cudaMemcpyDeviceToHost, s));
         FT_CUDA_TRY(cudaMemcpyAsync(h_nout, d_nout, (size_t)2 * S * 4, cudaMemcpyDeviceToHost, s));
+        phase_mark("d2h");
       }
       return FT_OK;
     }
@@ -752,6 +742,7 @@ struct ft_tracker {
       FT_CUDA_TRY(cudaMemcpyAsync(h_out, d_out, (size_t)S * 2 * cfg.max_tracks * sizeof(ft_track),
                                   cudaMemcpyDeviceToHost, s));
       FT_CUDA_TRY(cudaMemcpyAsync(h_nout, d_nout, (size_t)2 * S * 4, cudaMemcpyDeviceToHost, s));
+      phase_mark("d2h");
     }
     return FT_OK;
   }
@@ -759,18 +750,6 @@ struct ft_tracker {
   int run(bool has_prev, const uint8_t *luma, const ft_det *dets, const int32_t *in,
           bool host_io) {
     cudaStream_t s = stream;
-    const char *pt = getenv("FT_PHASE_TIMING");
-    if (pt && *pt == '1' && has_prev) {  // eager run with per-phase events
-      PhaseTimer timer;
-      timer.on = true;
-      timer.s = s;
-      g_phase = &timer;
-      const int rc = enqueue(s, has_prev, luma, dets, in, host_io);
-      g_phase = nullptr;
-      timer.report();
-      if (rc == FT_OK) pyr_par ^= 1;
-      return rc;
-    }
     // host-I/O graphs bake the staging slot's pinned pointers into their
     // copy nodes: key them by those pointers (one graph per slot)
     GraphKey key{(has_prev ? 1 : 0) | (pyr_par << 1), host_io ? (const void *)h_luma : luma,
@@ -778,6 +757,9 @@ struct ft_tracker {
     auto it = graphs.find(key);
     if (it == graphs.end()) {
       Graph g;
+      g.phases.reset(new PhaseRec());
+      for (auto &e : g.phases->ev) FT_CUDA_TRY(cudaEventCreate(&e));
+      g.phases->s = s;
       LaunchCounter lc;
       g_launch_counter = &lc;
       cudaGraph_t graph = nullptr;
@@ -787,8 +769,10 @@ struct ft_tracker {
         return cuda_fail(e, "cudaStreamBeginCapture");
       }
       g_pd_span = span.ev[0] ? &span : nullptr;
+      g_phase = g.phases.get();
       int rc = enqueue(s, has_prev, luma, dets, in, host_io);
       g_pd_span = nullptr;
+      g_phase = nullptr;
       e = cudaStreamEndCapture(s, &graph);
       g_launch_counter = nullptr;
       if (rc != FT_OK) {
@@ -800,10 +784,11 @@ struct ft_tracker {
       cudaGraphDestroy(graph);
       if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
       g.launches = lc.n;
-      it = graphs.emplace(key, g).first;
+      it = graphs.emplace(key, std::move(g)).first;
     }
     FT_CUDA_TRY(cudaGraphLaunch(it->second.exec, s));
     last_launches = it->second.launches;
+    last_graph = &it->second;
     pyr_par ^= 1;
     return FT_OK;
   }
@@ -957,7 +942,11 @@ int ft_tracker_destroy(ft_tracker *t) {
   if (!t) return FT_OK;
   DeviceGuard g(t->ctx->device);
   cudaStreamSynchronize(t->stream);
-  for (auto &kv : t->graphs) cudaGraphExecDestroy(kv.second.exec);
+  for (auto &kv : t->graphs) {
+    cudaGraphExecDestroy(kv.second.exec);
+    for (auto &e : kv.second.phases->ev)
+      if (e) cudaEventDestroy(e);
+  }
   for (void *p : t->allocs) cudaFree(p);
   flow_work_free(t->fw);
   for (auto &sl : t->slots) {
@@ -1010,6 +999,7 @@ int ft_tracker_submit(ft_tracker *t, int slot, int frame, const uint8_t *luma, c
   t->use_slot(slot);
   FT_TRY(t->join_in());
   FT_TRY(t->run(t->frames_seen > 0, nullptr, nullptr, nullptr, true));
+  sl.graph = t->last_graph;
   FT_CUDA_TRY(cudaEventRecord(sl.done, t->stream));
   FT_TRY(t->join_out());
   sl.pending = true;
@@ -1147,6 +1137,28 @@ int ft_tracker_pd_span(ft_tracker *t, double *ms, int *launches, double *pixel_i
   *ms = tot;
   *launches = t->span.launches;
   *pixel_iters = (double)t->span.pixel_iters;
+  return FT_OK;
+}
+
+int ft_tracker_phase_times(ft_tracker *t, int slot, double *ms, const char **names, int max,
+                           int *n) {
+  if (!t || !n || (max > 0 && !ms)) return fail(FT_EINVAL, "NULL argument");
+  if (slot < -1 || slot > 1) return fail(FT_EINVAL, "slot must be -1, 0 or 1");
+  DeviceGuard g(t->ctx->device);
+  const ft_tracker::Graph *gr =
+      slot < 0 ? t->last_graph : static_cast<const ft_tracker::Graph *>(t->slots[slot].graph);
+  *n = 0;
+  if (!gr) return FT_OK;
+  const PhaseRec &p = *gr->phases;
+  if (p.n < 2) return FT_OK;
+  FT_CUDA_TRY(cudaEventSynchronize(p.ev[p.n - 1]));
+  for (int i = 1; i < p.n && *n < max; ++i) {
+    float m = 0.f;
+    FT_CUDA_TRY(cudaEventElapsedTime(&m, p.ev[i - 1], p.ev[i]));
+    ms[*n] = m;
+    if (names) names[*n] = p.name[i];
+    ++*n;
+  }
   return FT_OK;
 }
 

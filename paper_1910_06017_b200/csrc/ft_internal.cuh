@@ -101,23 +101,23 @@ inline void count_launch(int n = 1) {
   if (g_launch_counter) g_launch_counter->n += n;
 }
 
-// Optional phase timing (FT_PHASE_TIMING=1): the tracker runs eagerly and
-// records a CUDA event at every mark(); report() prints the gaps to stderr.
-struct PhaseTimer {
-  bool on = false;
-  cudaStream_t s = nullptr;
+// Per-phase timing of a tracker step (SPEC.md:402-405 FrameResult timings):
+// while a step graph is captured, phase_mark() records an external CUDA
+// event node at every phase boundary; the events then hold the most recent
+// replay of that graph, and the gaps are the phases' device times.
+struct PhaseRec {
+  static constexpr int kMax = 16;
+  cudaEvent_t ev[kMax] = {};
+  const char *name[kMax] = {};
   int n = 0;
-  cudaEvent_t ev[64];
-  const char *name[64];
+  cudaStream_t s = nullptr;
   void mark(const char *what) {
-    if (!on || n >= 64) return;
-    cudaEventCreate(&ev[n]);
-    cudaEventRecord(ev[n], s);
+    if (n >= kMax || !ev[n]) return;
+    cudaEventRecordWithFlags(ev[n], s, cudaEventRecordExternal);
     name[n++] = what;
   }
-  void report();
 };
-extern PhaseTimer *g_phase;
+extern thread_local PhaseRec *g_phase;
 
 // Live timing of the dominant kernel inside the tracker step (bench.py's
 // roofline): run_flow records an event before the first and after the last

@@ -124,47 +124,6 @@ __device__ __forceinline__ double div_at(const double *__restrict__ px,
   return dx + dy;
 }
 
-constexpr int kRB = 32;  // ROF tile (kRB x kRB outputs, one halo row/col)
-
-// One ROF dual step (imaging.py:120-124):
-//   d = div(p) - img/weight;  g = forward_gradient(d);
-//   norm = 1 + step*hypot(g);  p = (p + step*g) / norm
-// d is staged in shared memory for the (kRB+1)^2 patch the tile needs.
-__global__ void __launch_bounds__(256) k_rof_step(const double *__restrict__ img, int w, int h,
-                                                  int64_t is, const double *__restrict__ px,
-                                                  const double *__restrict__ py,
-                                                  double *__restrict__ qx,
-                                                  double *__restrict__ qy, int64_t ps,
-                                                  double weight, double step) {
-  __shared__ double sd[kRB + 1][kRB + 2];
-  img += blockIdx.z * is;
-  px += blockIdx.z * ps;
-  py += blockIdx.z * ps;
-  qx += blockIdx.z * ps;
-  qy += blockIdx.z * ps;
-  const int c0 = blockIdx.x * kRB, r0 = blockIdx.y * kRB;
-  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
-  for (int k = tid; k < (kRB + 1) * (kRB + 1); k += blockDim.x * blockDim.y) {
-    const int lr = k / (kRB + 1), lc = k % (kRB + 1);
-    const int r = r0 + lr, c = c0 + lc;
-    double v = 0.0;
-    if (r < h && c < w) v = div_at(px, py, r, c, w, h) - img[(int64_t)r * w + c] / weight;
-    sd[lr][lc] = v;
-  }
-  __syncthreads();
-  for (int lr = threadIdx.y; lr < kRB; lr += blockDim.y) {
-    const int r = r0 + lr, c = c0 + threadIdx.x;
-    if (r >= h || c >= w) continue;
-    const double d = sd[lr][threadIdx.x];
-    const double gx = c < w - 1 ? sd[lr][threadIdx.x + 1] - d : 0.0;
-    const double gy = r < h - 1 ? sd[lr + 1][threadIdx.x] - d : 0.0;
-    const double norm = 1.0 + step * glibc_hypot(gx, gy);
-    const int64_t o = (int64_t)r * w + c;
-    qx[o] = (px[o] + step * gx) / norm;
-    qy[o] = (py[o] + step * gy) / norm;
-  }
-}
-
 // structure = img - weight*div(p); out = clip(((img - S) + blend*S +
 // (1-blend)) / (2-blend), 0, 1)   (imaging.py:125, :139-144)
 __global__ void k_st_combine(const double *__restrict__ img, int w, int h, int64_t is,
@@ -193,24 +152,20 @@ __global__ void k_st_combine(const double *__restrict__ img, int w, int h, int64
   out[o] = m;
 }
 
-// ROF iterations, temporally blocked (same scheme as k_pd_tile): a 32x32
+// ROF iterations, temporally blocked (same scheme as k_pd_tile): a 64x32
 // tile with `halo` overlap runs `iters` dual steps on chip; the two fields
 // read at a neighbour (p at x-1 / y-1 for the divergence, d at x+1 / y+1 for
-// the forward gradient) live in shared memory with a one-element apron,
-// img/weight and the own p in registers.  Exact inner region written back.
-constexpr int kRTW = 32, kRPY = 2;
-// BY warps per CTA: 16 (32x32 tiles, 2 CTAs/SM) or 32 (32x64 tiles, one CTA);
-// NXC columns per thread: 2 (64-wide tiles, the default: the halo columns
-// are 8 of 64 instead of 8 of 32; measured +1.3 % default / +7 % light
-// frames/s) or 1 (32-wide, FT_ROF_WIDE=0)
+// the forward gradient) live in shared memory with a one-element apron, the
+// own p in registers, img/weight in a fourth shared plane read only by its
+// owner (keeps the kernel free of spills).  Exact inner region written back.
+constexpr int kRPY = 2;
+// BY warps per CTA, NXC columns per thread: 16 x 2 = 64-wide tiles (the
+// halo columns are 8 of 64 instead of 8 of 32: measured +1.3 % default /
+// +7 % light frames/s over 32x32)
 template <int BY, int NXC = 1>
 struct RofGeom {
   static constexpr int TW = 32 * NXC, SP = TW + 2, TH = BY * kRPY, PL = SP * (TH + 2);
-#ifndef FT_ROF_IWREG
-  static constexpr size_t smem = 4 * PL * sizeof(double);  // + img/weight plane
-#else
-  static constexpr size_t smem = 3 * PL * sizeof(double);
-#endif
+  static constexpr size_t smem = 4 * PL * sizeof(double);  // px, py, d, img/weight
 };
 
 // FIX: halo 4 with 4 iterations per launch (every launch of the default 40
@@ -239,17 +194,9 @@ __device__ __forceinline__ void rof_tile_body(
   }
   __syncthreads();
   // element q: row ty + kRBY*(q / NXC), column tx + 32*(q % NXC)
-#ifndef FT_ROF_IWREG
-  // img/weight in a fourth shared plane, read by its owner only: frees 4
-  // doubles of registers (the 64x32 instantiation no longer spills;
-  // -DFT_ROF_IWREG keeps it in registers)
-  double *const s_iw = rof_sm + 3 * kRPL;
+  double *const s_iw = rof_sm + 3 * kRPL;  // img / weight, read by its owner only
 #define ROF_IW(q, id) s_iw[id]
   double px[NQ], py[NQ];
-#else
-#define ROF_IW(q, id) iw[q]
-  double iw[NQ], px[NQ], py[NQ];
-#endif
   bool fR[NQ], fD[NQ], fL[NQ], fLC[NQ], fU[NQ], fLR[NQ];
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
@@ -329,189 +276,12 @@ __global__ void __launch_bounds__(32 * kRBY, kRBY == 16 ? 2 : 1)
   using G = RofGeom<kRBY, NXC>;
   const int hh = FIX ? 4 : halo;
   const int ox = blockIdx.x * (G::TW - 2 * hh) - hh, oy = blockIdx.y * (G::TH - 2 * hh) - hh;
-#ifndef FT_ROF_NO_IN
   if (ox >= 1 && ox + G::TW <= w - 1 && oy >= 1 && oy + G::TH <= h - 1)
     rof_tile_body<P2, FIX, kRBY, NXC, true>(img, w, h, is, px_in, py_in, px_out, py_out, ps,
                                             weight, step, halo, iters, first, cone_on);
   else
-#endif
     rof_tile_body<P2, FIX, kRBY, NXC, false>(img, w, h, is, px_in, py_in, px_out, py_out, ps,
                                              weight, step, halo, iters, first, cone_on);
-}
-
-// ROF row sweep (opt-in FT_ROF_SWEEP=1), the k_pd_sweep scheme applied to
-// the ROF dual iteration (imaging.py:120-124): one warp owns a 32-column
-// strip (lane = column, K halo columns per side) and a row segment, and
-// streams down the rows with the 2K half-steps of K iterations pipelined at
-// one-row lags -- stage 2k (A_k): d = div(p) - img/weight; stage 2k+1 (B_k):
-// p = (p + step*grad d) / (1 + step*|grad d|).  A stages run before B stages
-// within a step, so all stages of a step are independent; x neighbours by
-// shuffles, y neighbours from the lane's previous rows (register carries,
-// two alternating slots); rows clipped per stage to the segment's cone.
-// Every pixel needs hypot + two divisions, so no queue: no barriers at all.
-__device__ __forceinline__ void rof_cp8(double *dst, const double *src, bool valid) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 8 : 0));
-}
-
-struct RofSweepArgs {
-  const double *img;
-  int w, h;
-  int64_t is;
-  const double *px_in, *py_in;
-  double *px_out, *py_out;
-  int64_t ps;
-  double weight, step;
-  int first, seg;
-  signed char cA[16], cB[16];
-};
-
-template <bool P2, int K>
-__global__ void __launch_bounds__(32, 16) k_rof_sweep(const RofSweepArgs a) {
-  constexpr int NH = 2 * K, L = NH - 1, NSLOT = 4, PF = NSLOT - 3, CR = 8;
-  constexpr int STRIP = 32 - 2 * K;
-  static_assert(NH - 2 < CR, "iw ring too short");
-  __shared__ double ring[NSLOT][3][32];  // img, px, py of rows s-1 .. s+1+PF
-  __shared__ double iwr[CR][32];         // img/weight of the rows A stages read
-  const int lane = threadIdx.x;
-  const int W = a.w, H = a.h;
-  const int x = blockIdx.x * STRIP - K + lane;
-  const bool xin = x >= 0 && x < W;
-  const bool wr = xin && lane >= K && lane < 32 - K;
-  const bool fR = x < W - 1, fL = x > 0, fLC = x == W - 1;
-  const int y0 = blockIdx.y * a.seg, y1 = min(y0 + a.seg, H);
-  const double *img = a.img + blockIdx.z * a.is;
-  const int64_t po = blockIdx.z * a.ps;
-  const double step = a.step, weight = a.weight;
-  int lo[NH], hi[NH], s1 = 0;
-#pragma unroll
-  for (int j = 0; j < NH; ++j) {
-    lo[j] = max(y0 - (int)a.cA[j], 0);
-    hi[j] = min(y1 + (int)a.cB[j], H);
-    s1 = max(s1, hi[j] + j);
-  }
-  const int s0 = lo[0];
-  const int lr0 = max(lo[0] - 1, 0), lr1 = min(hi[0] + 1, H);
-  auto load_row = [&](int r) {
-    if (r < lr0 || r >= lr1) return;
-    const int sl = r & (NSLOT - 1);
-    const int64_t o = (int64_t)r * W + x;
-    rof_cp8(&ring[sl][0][lane], xin ? img + o : img, xin);
-    if (!a.first) {
-      rof_cp8(&ring[sl][1][lane], xin ? a.px_in + po + o : a.px_in, xin);
-      rof_cp8(&ring[sl][2][lane], xin ? a.py_in + po + o : a.py_in, xin);
-    }
-  };
-  auto rd = [&](int r, int f) -> double {
-    return (a.first && f) ? 0.0 : ring[r & (NSLOT - 1)][f][lane];
-  };
-  auto iw_row = [&](int r) { iwr[r & (CR - 1)][lane] = rd(r, 0) / weight; };  // imaging.py:121
-  load_row(s0 - 1);
-  load_row(s0);
-  load_row(s0 + 1);
-  asm volatile("cp.async.commit_group;\n" ::);
-  // carries: slot t = rows produced at steps with (s - s0) & 1 == t
-  double pX[K][2][2], dX[K][2];
-#pragma unroll
-  for (int k = 0; k < K; ++k)
-#pragma unroll
-    for (int t = 0; t < 2; ++t) pX[k][t][0] = pX[k][t][1] = dX[k][t] = 0.0;
-  int s = s0;
-  auto stepf = [&](auto slot) {
-    constexpr int PA = decltype(slot)::value, PB = PA ^ 1;
-    load_row(s + 1 + PF);
-    asm volatile("cp.async.commit_group;\n" ::);
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(PF) : "memory");
-    if (s == s0 && s0 < lr1) iw_row(s0);
-    double dF[K];
-    // ---- A stages: d = div(p) - img/weight at rows s - 2k
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int r = s - 2 * k;
-      double p1, p2, q2;  // px(r), py(r), py(r-1)
-      if (k == 0) {
-        p1 = rd(r, 1); p2 = rd(r, 2); q2 = rd(r - 1, 2);
-      } else {
-        p1 = pX[k - 1][PB][0]; p2 = pX[k - 1][PB][1]; q2 = pX[k - 1][PA][1];
-      }
-      const double l1 = __shfl_up_sync(0xffffffffu, p1, 1);
-      const bool U = r > 0, LR = r == H - 1;
-      const double dx = fL ? (fLC ? -l1 : p1 - l1) : p1;
-      const double dy = U ? (LR ? -q2 : p2 - q2) : p2;
-      dF[k] = (dx + dy) - iwr[r & (CR - 1)][lane];
-    }
-    if (s + 1 < lr1) iw_row(s + 1);
-    double pF[K][2];
-    // ---- B stages: p update at rows s - 2k - 1
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int r = s - 2 * k - 1;
-      const double dc = dX[k][PB], dd = dF[k];  // d(r), d(r+1)
-      const double dr = __shfl_down_sync(0xffffffffu, dc, 1);
-      double o1, o2;  // own p before the update
-      if (k == 0) { o1 = rd(r, 1); o2 = rd(r, 2); }
-      else { o1 = pX[k - 1][PA][0]; o2 = pX[k - 1][PA][1]; }
-      const bool D = r < H - 1;
-      const double gx = fR ? dr - dc : 0.0;
-      const double gy = D ? dd - dc : 0.0;
-      const double hy = glibc_hypot(gx, gy);
-      const double norm = P2 ? fma(step, hy, 1.0) : 1.0 + step * hy;
-      pF[k][0] = (P2 ? fma(step, gx, o1) : o1 + step * gx) / norm;
-      pF[k][1] = (P2 ? fma(step, gy, o2) : o2 + step * gy) / norm;
-    }
-    {
-      const int r = s - L;
-      if (r >= y0 && r < y1 && wr) {
-        const int64_t o = po + (int64_t)r * W + x;
-        a.px_out[o] = pF[K - 1][0];
-        a.py_out[o] = pF[K - 1][1];
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      dX[k][PA] = dF[k];
-      pX[k][PA][0] = pF[k][0];
-      pX[k][PA][1] = pF[k][1];
-    }
-    ++s;
-  };
-  while (s + 1 < s1) {
-    stepf(std::integral_constant<int, 0>{});
-    stepf(std::integral_constant<int, 1>{});
-  }
-  if (s < s1) stepf(std::integral_constant<int, 0>{});
-  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-}
-
-// stage cone of a (A B)xK sweep launch: B at [a,b) reads A at [a,b+1) and the
-// previous B at [a,b); A at [a,b) reads the previous B at [a-1,b)
-void rof_cone(int nh, signed char *cA, signed char *cB) {
-  int A[16], B[16];
-  for (int j = 0; j < 16; ++j) A[j] = B[j] = -1000;
-  auto cover = [&](int j, int x, int y) {
-    if (j < 0) return;
-    A[j] = std::max(A[j], x);
-    B[j] = std::max(B[j], y);
-  };
-  cover(nh - 1, 0, 0);
-  for (int j = nh - 1; j >= 0; --j) {
-    if (A[j] == -1000) continue;
-    if (j & 1) {
-      cover(j - 1, A[j], B[j] + 1);
-      cover(j - 2, A[j], B[j]);
-    } else {
-      cover(j - 1, A[j] + 1, B[j]);
-    }
-  }
-  for (int j = 0; j < 16; ++j) {
-    cA[j] = (signed char)(j < nh ? std::max(A[j], 0) : 0);
-    cB[j] = (signed char)(j < nh ? std::max(B[j], 0) : 0);
-  }
-}
-
-int getenv_int(const char *name, int dflt) {
-  const char *v = getenv(name);
-  return v && *v ? atoi(v) : dflt;
 }
 
 int grid1d(int64_t n, int bs) {
@@ -566,78 +336,33 @@ int launch_structure_texture(const double *img, int w, int h, int64_t is, double
   for (int b = 0; b < nb; ++b) FT_CUDA_TRY(cudaMemsetAsync(ws + b * wss, 0, 2 * n * 8, s));
   double *p[2][2] = {{ws, ws + n}, {ws + 2 * n, ws + 3 * n}};
   int cur = 0;
-  dim3 blk(32, 8), grd((w + kRB - 1) / kRB, (h + kRB - 1) / kRB, nb);
-  const char *naive = getenv("FT_ROF_NAIVE");
-  if (naive && *naive == '1') {  // one launch per iteration (A/B reference)
-    for (int it = 0; it < iterations; ++it) {
-      k_rof_step<<<grd, blk, 0, s>>>(img, w, h, is, p[cur][0], p[cur][1], p[1 - cur][0],
-                                     p[1 - cur][1], wss, weight, step);
-      count_launch();
-      cur = 1 - cur;
-    }
-  } else {
-    const char *hv = getenv("FT_ROF_HALO");
-    const int halo_t = (hv && *hv) ? atoi(hv) : 4;
-    const int tall = getenv_int("FT_ROF_TALL", 0);  // 32x64 tiles, 1024 threads
-    const int wide = getenv_int("FT_ROF_WIDE", 1);  // 64-wide tiles (default)
-    const int kRTH = tall ? RofGeom<32>::TH : RofGeom<16>::TH;
-    const int tw = wide ? RofGeom<16, 2>::TW : kRTW;
-    const bool resident = w <= tw && h <= kRTH;
-    const int halo = resident ? 0 : halo_t;
-    const char *cv = getenv("FT_ROF_CONE");
-    const int cone_on = (cv && *cv) ? atoi(cv) : 1;
-    const int sx = tw - 2 * halo, sy = kRTH - 2 * halo;
-    const dim3 g(resident ? 1 : (w + sx - 1) / sx, resident ? 1 : (h + sy - 1) / sy, nb);
-    int done = 0;
-    while (done < iterations) {
-      const int k = resident ? iterations : std::min(halo, iterations - done);
-      int e2 = 0;
-      const bool p2 = step > 0.0 && std::frexp(step, &e2) == 0.5;
-      if (!resident && k == 4 && getenv_int("FT_ROF_SWEEP", 0)) {
-        RofSweepArgs ra;
-        ra.img = img;
-        ra.w = w;
-        ra.h = h;
-        ra.is = is;
-        ra.px_in = p[cur][0];
-        ra.py_in = p[cur][1];
-        ra.px_out = p[1 - cur][0];
-        ra.py_out = p[1 - cur][1];
-        ra.ps = wss;
-        ra.weight = weight;
-        ra.step = step;
-        ra.first = done == 0;
-        ra.seg = std::max(1, getenv_int("FT_ROF_SWEEP_SEG", 64));
-        rof_cone(8, ra.cA, ra.cB);
-        const dim3 gs((w + 23) / 24, (h + ra.seg - 1) / ra.seg, nb);
-        if (p2) k_rof_sweep<true, 4><<<gs, 32, 0, s>>>(ra);
-        else k_rof_sweep<false, 4><<<gs, 32, 0, s>>>(ra);
-        count_launch();
-        cur = 1 - cur;
-        done += k;
-        continue;
-      }
-      const bool fix = !resident && halo == 4 && k == 4 && cone_on && getenv_int("FT_ROF_FIX", 1);
-      auto kern = tall && wide ? (p2 ? (fix ? k_rof_tile<true, true, 32, 2> : k_rof_tile<true, false, 32, 2>)
-                                     : (fix ? k_rof_tile<false, true, 32, 2> : k_rof_tile<false, false, 32, 2>))
-                  : tall ? (p2 ? (fix ? k_rof_tile<true, true, 32> : k_rof_tile<true, false, 32>)
-                             : (fix ? k_rof_tile<false, true, 32> : k_rof_tile<false, false, 32>))
-                  : wide ? (p2 ? (fix ? k_rof_tile<true, true, 16, 2> : k_rof_tile<true, false, 16, 2>)
-                               : (fix ? k_rof_tile<false, true, 16, 2> : k_rof_tile<false, false, 16, 2>))
-                       : (p2 ? (fix ? k_rof_tile<true, true> : k_rof_tile<true>)
-                             : (fix ? k_rof_tile<false, true> : k_rof_tile<false>));
-      const size_t rsm = tall ? (wide ? RofGeom<32, 2>::smem : RofGeom<32>::smem)
-                              : wide ? RofGeom<16, 2>::smem : RofGeom<16>::smem;
-      if (rsm > 48 * 1024)
-        FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
-      kern<<<g, dim3(32, tall ? 32 : 16), rsm, s>>>(img, w, h, is, p[cur][0], p[cur][1], p[1 - cur][0],
-                                        p[1 - cur][1], wss, weight, step, halo, k, done == 0,
-                                        cone_on);
-      count_launch();
-      cur = 1 - cur;
-      done += k;
-    }
+  // 64x32 tiles (16 warps, 2 columns x 2 rows per thread), halo 4, 4
+  // iterations per launch; a level that fits one tile runs all iterations
+  // in one launch without halo.  Measured alternatives (32x32, 32x64, 64x64
+  // tiles, a row-sweep kernel, one launch per iteration) are in DESIGN.md.
+  using G = RofGeom<16, 2>;
+  const bool resident = w <= G::TW && h <= G::TH;
+  const int halo = resident ? 0 : 4;
+  const int sx = G::TW - 2 * halo, sy = G::TH - 2 * halo;
+  const dim3 g(resident ? 1 : (w + sx - 1) / sx, resident ? 1 : (h + sy - 1) / sy, nb);
+  int e2 = 0;
+  const bool p2 = step > 0.0 && std::frexp(step, &e2) == 0.5;
+  int done = 0;
+  while (done < iterations) {
+    const int k = resident ? iterations : std::min(halo, iterations - done);
+    const bool fix = !resident && k == 4;
+    auto kern = p2 ? (fix ? k_rof_tile<true, true, 16, 2> : k_rof_tile<true, false, 16, 2>)
+                   : (fix ? k_rof_tile<false, true, 16, 2> : k_rof_tile<false, false, 16, 2>);
+    FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)G::smem));
+    kern<<<g, dim3(32, 16), G::smem, s>>>(img, w, h, is, p[cur][0], p[cur][1], p[1 - cur][0],
+                                          p[1 - cur][1], wss, weight, step, halo, k, done == 0,
+                                          1);
+    count_launch();
+    cur = 1 - cur;
+    done += k;
   }
+  const dim3 blk(32, 8);
   dim3 g2((w + 31) / 32, (h + 7) / 8, nb);
   k_st_combine<<<g2, blk, 0, s>>>(img, w, h, is, p[cur][0], p[cur][1], wss, weight, blend, out,
                                   os, mode);

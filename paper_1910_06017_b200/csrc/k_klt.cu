@@ -335,18 +335,11 @@ int launch_klt_predict(const KltArgs &a, const double *boxes, double *out_boxes,
   if (a.grid < 1 || a.grid * a.grid > 128) return fail(FT_EINVAL, "klt grid must be 1..11");
   const int items = max_boxes * a.grid * a.grid;
   if (items == 0) return FT_OK;
-  // resident CTAs per SM requested from ptxas (register cap); FT_KLT_MINB
-  static const int minb = [] {
-    const char *e = getenv("FT_KLT_MINB");
-    return e ? atoi(e) : 3;
-  }();
+  // 3 resident CTAs per SM requested from ptxas (register cap; 2 and 4
+  // measured slower)
   const dim3 grid((items + kPtWarps - 1) / kPtWarps, n_streams);
-  if (minb >= 4)
-    k_klt_points<4><<<grid, 32 * kPtWarps, 0, s>>>(a, boxes, box_stride, n_boxes, n_boxes_const, pts, fwd, fb);
-  else if (minb == 3)
-    k_klt_points<3><<<grid, 32 * kPtWarps, 0, s>>>(a, boxes, box_stride, n_boxes, n_boxes_const, pts, fwd, fb);
-  else
-    k_klt_points<2><<<grid, 32 * kPtWarps, 0, s>>>(a, boxes, box_stride, n_boxes, n_boxes_const, pts, fwd, fb);
+  k_klt_points<3><<<grid, 32 * kPtWarps, 0, s>>>(a, boxes, box_stride, n_boxes, n_boxes_const, pts,
+                                                 fwd, fb);
   k_klt_boxes<<<dim3((max_boxes + kPtWarps - 1) / kPtWarps, n_streams), 32 * kPtWarps, 0, s>>>(
       a, boxes, out_boxes, box_stride, n_boxes, n_boxes_const, pts, fwd, fb, valid, frame_w,
       frame_h);

@@ -143,6 +143,9 @@ class Tracker:
         """One frame for every stream; returns a list (per stream) of
         TRACK_DTYPE record arrays: the active tracks in scene order followed
         by the tracks that turned Lost this frame."""
+        if self._pending:  # slot 0's pinned inputs may still feed an in-flight step
+            raise RuntimeError(f"{len(self._pending)} submitted step(s) in flight: call wait() "
+                               "before a synchronous step")
         self._stage(frames, detections)
         _lib.check(self._lib.ft_tracker_step(
             self._h, _lib.ptr(self.luma_in), int(frame_index), _lib.ptr(self.dets_in),
@@ -224,6 +227,83 @@ class Tracker:
         c = C.c_int64()
         _lib.check(self._lib.ft_tracker_launches(self._h, C.byref(c)))
         return c.value
+
+    def phase_ms(self, slot: int = -1) -> dict:
+        """Per-phase device times (ms) of a step: slot 0/1 =
+        the step last submitted in that slot, -1 = the most recent step.
+        Keys in execution order ("h2d", "ingest+pyramid", "structure_texture",
+        "flow pyramid", "flow level k" ..., "predict+match+update", "d2h")."""
+        n = C.c_int()
+        ms = (C.c_double * 32)()
+        names = (C.c_char_p * 32)()
+        _lib.check(self._lib.ft_tracker_phase_times(self._h, int(slot), ms, names, 32,
+                                                    C.byref(n)))
+        out = {}
+        for i in range(n.value):
+            k = names[i].decode()
+            out[k] = round(out.get(k, 0.0) + ms[i], 4)
+        return out
+
+    def pd_span(self):
+        """Live device time of the finest-level primal-dual launches of the
+        most recent step: (ms, launches, pixel-iterations over all streams)."""
+        ms, n, pi = C.c_double(), C.c_int(), C.c_double()
+        _lib.check(self._lib.ft_tracker_pd_span(self._h, C.byref(ms), C.byref(n), C.byref(pi)))
+        return ms.value, n.value, pi.value
+
+    def roofline(self, hbm_peak, frame_bytes: float, step_ms: float,
+                 frames_per_s_per_gpu: float, profiles_dir: str) -> dict:
+        """Roofline of the dominant kernel (finest-level primal-dual launches)
+        from the live in-graph timing of the last step, against the HBM peak
+        (SURVEY 8(d)'s streaming model: 152 algorithmic bytes per
+        pixel-iteration) AND the resources that actually bind it: DRAM bytes
+        of this build per launch (ncu, profiles/pd_profile.json), useful fp64
+        operations against the measured fp64 peak, ncu issue-slot use."""
+        import json
+        import os
+        hbm, peak_src = hbm_peak
+        ms, n, pix_it = self.pd_span()
+        if ms <= 0 or n == 0:
+            return None
+        sec = ms / 1000.0
+        achieved = 152.0 * pix_it / sec / 1e9
+        prof = {}
+        pf = os.path.join(profiles_dir, "pd_profile.json")
+        if os.path.exists(pf):
+            prof = json.load(open(pf))
+        fp = os.path.join(profiles_dir, "fp64_peak.json")
+        fp64_peak = json.load(open(fp))["dadd_dmul_ops_per_s"] if os.path.exists(fp) else None
+        # reference arithmetic per pixel-iteration (optflow.py:180-208):
+        # dual 4 differences + 12 mul/add + 2 hypot + 4 divisions, primal
+        # 6 divergence + 4 + 4 (rho) + 2 + 4 + 4 (u-bar) = 46 fp64 ops
+        ops = 46.0 * pix_it
+        sp = self.width * self.height  # noqa: F841 (frame size, for the record)
+        pixels = pix_it / max(self.flow_params.iterations_per_warp, 1) / \
+            max(self.flow_params.warps_per_level, 1)
+        dram = None
+        if prof.get("dram_bytes_per_stream_pixel_per_launch"):
+            dram = prof["dram_bytes_per_stream_pixel_per_launch"] * pixels * n
+        out = {"bound": "hbm", "kernel": prof.get("kernel", "k_pd_tile (TV-L1 primal-dual, finest level)"),
+               "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+               "frac": round(achieved / hbm, 4),
+               "traffic": round(dram / n, 1) if dram else None,
+               "timing": "live: CUDA events in the step graph around the finest-level primal-dual "
+                         "launches of the last timed step",
+               "launches": n, "ms_per_launch": round(ms / n, 5),
+               "algorithmic_bytes_per_launch": 152.0 * pix_it / n,
+               "compulsory_bytes_per_launch": prof.get("compulsory_bytes_per_stream_pixel", 120.0)
+               * pixels,
+               "share_of_step": round(ms / step_ms, 4) if step_ms else None,
+               "dram_frac": round(dram / sec / 1e9 / hbm, 4) if dram else None,
+               "fp64_frac": round(ops / sec / fp64_peak, 4) if fp64_peak else None,
+               "fp64_ops_per_pixel_iter": 46,
+               "fp64_peak_ops_per_s": fp64_peak,
+               "issue_frac": prof.get("issue_slots_busy"),
+               "ncu_source": prof.get("source"),
+               "peak_source": peak_src,
+               "step_roofline_frac": round(frames_per_s_per_gpu * frame_bytes / (hbm * 1e9), 4),
+               "step_bytes_per_frame": frame_bytes}
+        return out
 
 
 

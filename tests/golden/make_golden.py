@@ -299,6 +299,104 @@ def gen_io():
     save("io.npz", **out)
 
 
+# ---- headline workload end to end (VERDICT r01 "next" #1) -------------------
+# bench.py's own C2 streams (global stream id s -> seed 1000 + s), 720x576,
+# 100 objects with scale change, detections every 5th frame with 1 px jitter,
+# default FlowParams, through t = 10: two full-size match/update rounds after
+# tracked frames.  ST and flow pairs do not depend on track state
+# (imaging.py:128-144, optflow.py:217-253), so they run in a process pool; the
+# per-stream predict/match/update chain then runs sequentially.
+C2_STREAMS, C2_FRAMES, C2_W, C2_H, C2_OBJ, C2_EVERY = 4, 11, 720, 576, 100, 5
+C2_FIELD_STRIDE = 16  # subsampled fields stored (full SD fields are 3.3 MB each)
+
+
+def _c2_seq(s):
+    return make_sequence(C2_W, C2_H, C2_OBJ, C2_FRAMES, seed=1000 + s, det_every=C2_EVERY,
+                         scale_change=True, jitter=1.0)
+
+
+def _c2_st(job):
+    s, t = job
+    frames, _ = _c2_seq(s)
+    u8 = frames[t]
+    H, W = u8.shape
+    L = imaging.select_level(W, H)
+    lvl = imaging.build_pyramid(imaging.Frame.from_gray8(u8, index=t), L + 1).levels[L]
+    return imaging.structure_texture(lvl).data
+
+
+def _c2_flow(job):
+    a, b, t = job
+    fa = imaging.Frame.from_array(a, t - 1)
+    fb = imaging.Frame.from_array(b, t)
+    fld = optflow.compute_flow(fa, fb, optflow.FlowParams())
+    return fld.dx, fld.dy
+
+
+def gen_c2():
+    import hashlib
+    import multiprocessing as mp
+    import time
+    t0 = time.time()
+    n = C2_STREAMS
+    with mp.get_context("fork").Pool(min(os.cpu_count() or 1, 16)) as pool:
+        sts = pool.map(_c2_st, [(s, t) for s in range(n) for t in range(C2_FRAMES)])
+        st = {(s, t): sts[s * C2_FRAMES + t] for s in range(n) for t in range(C2_FRAMES)}
+        print(f"  ST done {time.time() - t0:.0f}s", flush=True)
+        jobs = [(st[(s, t - 1)], st[(s, t)], t) for s in range(n) for t in range(1, C2_FRAMES)]
+        flows = pool.map(_c2_flow, jobs)
+        print(f"  flow done {time.time() - t0:.0f}s", flush=True)
+    out = {"cfg": np.array([C2_W, C2_H, C2_OBJ, C2_FRAMES, C2_EVERY, n, C2_FIELD_STRIDE])}
+    k = 0
+    for s in range(n):
+        frames, dets = _c2_seq(s)
+        out[f"s{s}_frames_sha"] = np.frombuffer(hashlib.sha256(frames.tobytes()).digest(), np.uint8)
+        L = imaging.select_level(C2_W, C2_H)
+        scene = []
+        margin = np.inf
+        for t in range(C2_FRAMES):
+            d = dets[t]
+            if d is not None:
+                d = detect.filter_detections(d, 0.5)
+            arr, nd = dets_to_arr(dets[t])
+            out[f"s{s}_d{t}"] = arr
+            out[f"s{s}_n{t}"] = np.array([nd])
+            if t == 0:
+                if d is not None:
+                    scene = track.update([], assoc.Assignment((), (), tuple(range(len(d)))), d, t)
+            else:
+                dx, dy = flows[k]
+                k += 1
+                fld = optflow.MotionField(width=C2_W >> L, height=C2_H >> L, dx=dx, dy=dy,
+                                          frame_index=t)
+                out[f"s{s}_dx{t}"] = dx[::C2_FIELD_STRIDE, ::C2_FIELD_STRIDE].copy()
+                out[f"s{s}_dy{t}"] = dy[::C2_FIELD_STRIDE, ::C2_FIELD_STRIDE].copy()
+                act = [i for i, o in enumerate(scene) if o.state == track.ACTIVE]
+                pred = track.predict([scene[i] for i in act], fld, L, (C2_W, C2_H))
+                out[f"s{s}_valid{t}"] = np.array([p is not None for p in pred])
+                scene = list(scene)
+                for i, p in zip(act, pred):
+                    if p is not None:
+                        scene[i] = replace(scene[i], box=p)
+                if d is not None:
+                    cand = [i for i, p in zip(act, pred) if p is not None]
+                    objs = [scene[i] for i in cand]
+                    for o in objs:  # near-tie exposure: min |iou - gate|
+                        for dd in d:
+                            if o.class_id == dd.class_id:
+                                margin = min(margin, abs(assoc.iou(o.box, dd.box) - 0.3))
+                    a = assoc.match(objs, d, 0.3)
+                    out[f"s{s}_pairs{t}"] = np.array([(cand[i], j) for i, j, _ in a.pairs],
+                                                     dtype=np.int64).reshape(-1, 2)
+                    pairs = tuple((cand[i], j, sc) for i, j, sc in a.pairs)
+                    scene = track.update(scene, assoc.Assignment(pairs, (), a.unmatched_detections),
+                                         d, t)
+            out[f"s{s}_scene{t}"] = scene_to_arr(scene)
+        out[f"s{s}_min_gate_margin"] = np.array([margin])
+        print(f"  stream {s}: {len(scene)} objects, min |iou-gate| {margin:.3e}", flush=True)
+    save("c2_tracks.npz", **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["imaging", "flow", "predict", "assoc", "step", "io"]
     for w in which:

@@ -66,3 +66,45 @@ def test_c4_uhd_500_tracks():
     act = _run(3840, 2160, 500, 2, seed=1003, det_every=1, scale_change=True, jitter=1.0,
                warps=1, iters=4, scales=5)
     assert act[-1] > 250
+
+
+def test_c5_headline_batch_matches_live_reference():
+    """The headline workload itself, pinned end to end to the LIVE reference:
+    bench.py's 64-stream C5 batch (global stream id s -> seed 1000 + s;
+    720x576, 100 objects with scale change, detections every 5th frame,
+    1 px jitter, default FlowParams) through t = 10.  Streams 0-3 are
+    compared bit-exactly at every frame against tests/golden/c2_tracks.npz
+    (tests/golden/make_golden.py:gen_c2 composed flowtrack's own functions,
+    optflow.py:217-253, track.py:56-139, assoc.py:109-135): track tables,
+    predict-None masks, match pairs (via the tables) and the motion field on
+    a 16-px lattice.  Two full-size match/update rounds follow tracked
+    frames (t = 5, 10)."""
+    import hashlib
+    import os
+
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("gpu tests need a CUDA device")
+    import bench
+    from paper_1910_06017_b200.pipeline import Tracker
+    from paper_1910_06017_b200.synth import make_sequence
+    from tests.goldutil import step_dets  # noqa: F401  (fixture layout shared)
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "c2_tracks.npz"))
+    W, H, n_obj, T, every, n_pin, stride = (int(v) for v in z["cfg"])
+    B = 64
+    seqs = [make_sequence(W, H, n_obj, T, seed=bench.stream_seed(s), det_every=every,
+                          scale_change=True, jitter=1.0) for s in range(B)]
+    for s in range(n_pin):
+        sha = hashlib.sha256(seqs[s][0].tobytes()).digest()
+        assert sha == z[f"s{s}_frames_sha"].tobytes(), f"synthetic stream {s} drifted"
+    trk = Tracker(W, H, n_streams=B, max_tracks=256, max_dets=160)
+    for t in range(T):
+        frames = np.stack([seqs[s][0][t] for s in range(B)])
+        scenes = trk.step(frames, t, [seqs[s][1][t] for s in range(B)])
+        for s in range(n_pin):
+            assert np.array_equal(scene_rows(scenes[s]), z[f"s{s}_scene{t}"]), (s, t)
+            if t > 0:
+                dx, dy = trk.field(s)
+                assert np.array_equal(dx[::stride, ::stride], z[f"s{s}_dx{t}"]), (s, t)
+                assert np.array_equal(dy[::stride, ::stride], z[f"s{s}_dy{t}"]), (s, t)
+    trk.close()

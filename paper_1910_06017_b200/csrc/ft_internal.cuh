@@ -173,8 +173,12 @@ struct FlowWork {
   double *ix = nullptr, *iy = nullptr;
   // primal-dual state, ping-pong (8 planes each: u1 u2 b1 b2 p11 p12 p21 p22)
   double *st[2] = {nullptr, nullptr};
-  // flow at the current level (u1,u2) and at the previous (coarser) level
-  double *u_prev = nullptr;  // 2 planes
+  // whole-level primal-dual path (k_pd_level.cu): CTAs one cooperative
+  // launch holds on this device (0: unavailable), tile edge exchange records,
+  // half-step flags, timeout flag
+  int level_ctas = 0;
+  void *edges = nullptr;
+  unsigned *flags = nullptr, *err = nullptr;
 };
 int flow_work_alloc(FlowWork &fw, int nb, int64_t cap);
 void flow_work_free(FlowWork &fw);
@@ -182,6 +186,7 @@ void flow_work_free(FlowWork &fw);
 struct FlowParamsD {
   double lam, tau, eps;
   int warps, iters;
+  int pd_kernel = FT_PD_AUTO;  // FT_PD_AUTO: whole-level kernel where a level fits; FT_PD_TILED
 };
 
 // Coarse-to-fine TV-L1 over nb image pairs given their (already scaled x255)

@@ -18,6 +18,7 @@
 #include <type_traits>
 
 #include "ft_internal.cuh"
+#include "ft_pd_level.cuh"
 
 namespace ft {
 
@@ -741,11 +742,27 @@ int flow_work_alloc(FlowWork &fw, int nb, int64_t cap) {
   fw.iy = all + 4 * pe;
   fw.st[0] = all + 5 * pe;
   fw.st[1] = all + (5 + NST) * pe;
+  // whole-level primal-dual path: exchange records + flags for the CTAs one
+  // cooperative launch holds on this device
+  int dev = 0;
+  FT_CUDA_TRY(cudaGetDevice(&dev));
+  FT_TRY(level_pd_capacity(dev, &fw.level_ctas));
+  if (fw.level_ctas > 0) {
+    const size_t eb = level_pd_edges_bytes(fw.level_ctas);
+    char *x = nullptr;
+    e = cudaMalloc(&x, eb + (size_t)(2 * fw.level_ctas + 64) * sizeof(unsigned));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(level exchange)");
+    fw.edges = x;
+    fw.flags = reinterpret_cast<unsigned *>(x + eb);
+    fw.err = fw.flags + 2 * fw.level_ctas;
+    FT_CUDA_TRY(cudaMemset(fw.err, 0, sizeof(unsigned)));
+  }
   return FT_OK;
 }
 
 void flow_work_free(FlowWork &fw) {
   if (fw.gx) cudaFree(fw.gx);
+  if (fw.edges) cudaFree(fw.edges);
   fw = FlowWork();
 }
 
@@ -785,6 +802,11 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
     const PDPlan plan = pd_plan(w, h);
     const bool resident = plan.halo == 0;
     const int halo = plan.halo;
+    // whole-level kernel for tiled levels whose tiles fit one cooperative
+    // launch (at least one stream per launch)
+    const int level_batch =
+        fw.level_ctas > 0 ? fw.level_ctas / level_pd_tiles(w, h) : 0;
+    const bool level = !resident && p.pd_kernel == FT_PD_AUTO && level_batch >= 1;
     PdSpan *span = lvl == 0 && !resident ? g_pd_span : nullptr;
     if (span) span->spans = span->launches = 0, span->pixel_iters = 0;
     for (int wp = 0; wp < p.warps; ++wp) {
@@ -795,11 +817,42 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
       const int si = span && span->spans < PdSpan::kMaxSpans ? span->spans : -1;
       if (si >= 0)
         FT_CUDA_TRY(cudaEventRecordWithFlags(span->ev[2 * si], s, cudaEventRecordExternal));
+      if (level) {
+        // whole level on chip: one cooperative launch per batch of streams
+        StatePtrs in = state_ptrs(fw.st[cur], fw.nb, cap);
+        StatePtrs out = state_ptrs(fw.st[1 - cur], fw.nb, cap);
+        for (int b0 = 0; b0 < nb; b0 += level_batch) {
+          const int bn = std::min(level_batch, nb - b0);
+          const int64_t bo = (int64_t)b0 * cap;
+          LevelPDArgs la;
+          la.u1 = in.p[U1] + bo;
+          la.u2 = in.p[U2] + bo;
+          la.out1 = out.p[U1] + bo;
+          la.out2 = out.p[U2] + bo;
+          la.gx = fw.gx + bo;
+          la.gy = fw.gy + bo;
+          la.r0 = fw.r0 + bo;
+          la.w = w;
+          la.h = h;
+          la.cap = cap;
+          la.iters = p.iters;
+          la.tau = p.tau;
+          la.lam = p.lam;
+          la.sigma = sigma;
+          la.shrink = shrink;
+          la.edges = fw.edges;
+          la.flags = fw.flags;
+          la.err = fw.err;
+          FT_TRY(launch_level_pd(la, bn, pow2_params(p.tau), s));
+          if (si >= 0) ++span->launches;
+        }
+        cur = 1 - cur;
+      }
       // 2*iters half-steps D P D P ... split into launches that end after a
       // dual step (state u, p): the first of at most 2*halo-1 half-steps
       // (starts with D), then 2*halo (P..D), and the rest (odd, P..P) in the
       // last launch; a resident level runs them all in one launch.
-      const int total = 2 * p.iters;
+      const int total = level ? 0 : 2 * p.iters;
       int done = 0;
       while (done < total) {
         int n;

@@ -310,7 +310,7 @@ def run_ours(args, ws, rank, local):
 
     prm = _flow_params(args.flow)
     trk = Tracker(W_, H_, n_streams=B, flow_params=prm, max_tracks=max_tracks, max_dets=max_dets,
-                  device=local, motion=args.motion, klt_grid=10, pd_kernel=args.pd_kernel)
+                  device=local, motion=args.motion, klt_grid=10)
     stream = torch.cuda.current_stream(dev)
 
     # ---------------- device-resident timing (value) ----------------
@@ -462,8 +462,6 @@ def main():
                     help="tvl1: the reference path (headline); klt: SURVEY 8 f4 backend")
     ap.add_argument("--flow", choices=["default", "light"], default="default",
                     help="default FlowParams (headline) or SURVEY 8(d)'s light 2 warps x 10 iters")
-    ap.add_argument("--pd-kernel", choices=["auto", "tiled"], default="auto",
-                    help="primal-dual kernel of tiled levels (A/B only; identical results)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget-s", type=float, default=150.0)
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2",

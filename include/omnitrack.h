@@ -39,13 +39,7 @@ extern "C" {
 #define FT_ENOMEM (-4) /* device / pinned allocation failed */
 #define FT_ECAP (-5)   /* tracker capacity (max_tracks / max_dets) exceeded */
 
-/* optflow.py:36-66 FlowParams; pyramid_scales <= 0 means auto (optflow.py:96).
- * pd_kernel is a tuning field with no reference counterpart (results are
- * bit-identical either way): FT_PD_AUTO runs every tiled pyramid level with
- * the whole-level primal-dual kernel where the level fits one cooperative
- * launch, FT_PD_TILED always uses the temporally blocked tile kernel. */
-#define FT_PD_AUTO 0
-#define FT_PD_TILED 1
+/* optflow.py:36-66 FlowParams; pyramid_scales <= 0 means auto (optflow.py:96) */
 typedef struct ft_flow_params {
   double data_weight;   /* lambda, default 0.15 */
   double huber_epsilon; /* default 0.01 */
@@ -53,7 +47,7 @@ typedef struct ft_flow_params {
   int32_t warps_per_level;     /* default 5 */
   int32_t iterations_per_warp; /* default 50 */
   int32_t pyramid_scales;      /* <= 0: auto_scales */
-  int32_t pd_kernel;           /* FT_PD_AUTO (0) or FT_PD_TILED */
+  int32_t _pad;
 } ft_flow_params;
 
 typedef struct ft_ctx ft_ctx;

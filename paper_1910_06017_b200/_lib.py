@@ -26,7 +26,7 @@ class ft_flow_params(C.Structure):
     _fields_ = [("data_weight", C.c_double), ("huber_epsilon", C.c_double),
                 ("time_step", C.c_double), ("warps_per_level", C.c_int32),
                 ("iterations_per_warp", C.c_int32), ("pyramid_scales", C.c_int32),
-                ("pd_kernel", C.c_int32)]
+                ("_pad", C.c_int32)]
 
 
 class ft_det(C.Structure):
@@ -177,14 +177,7 @@ def ptr(a) -> C.c_void_p:
     return C.c_void_p(a.ctypes.data)
 
 
-PD_KERNELS = {"auto": 0, "tiled": 1}  # ft_flow_params.pd_kernel (FT_PD_AUTO / FT_PD_TILED)
-
-
-def flow_params_struct(p, pd_kernel: str = "auto") -> ft_flow_params:
-    """FlowParams -> ft_flow_params.  pd_kernel is a tuning choice with
-    bit-identical results: "auto" (whole-level primal-dual kernel where a
-    level fits one cooperative launch) or "tiled" (always the tile kernel)."""
+def flow_params_struct(p) -> ft_flow_params:
     return ft_flow_params(float(p.data_weight), float(p.huber_epsilon), float(p.time_step),
                           int(p.warps_per_level), int(p.iterations_per_warp),
-                          0 if p.pyramid_scales is None else int(p.pyramid_scales),
-                          PD_KERNELS[pd_kernel])
+                          0 if p.pyramid_scales is None else int(p.pyramid_scales), 0)

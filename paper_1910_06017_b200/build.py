@@ -17,8 +17,8 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libomnitrack.so")
 ROOT = os.path.dirname(HERE)
 
-SOURCES = ["ft_api.cu", "k_imaging.cu", "k_flow.cu", "k_pd_level.cu", "k_track.cu", "k_klt.cu"]
-HEADERS = ["ft_internal.cuh", "ft_tracker.cuh", "ft_klt.cuh", "ft_pd_level.cuh"]
+SOURCES = ["ft_api.cu", "k_imaging.cu", "k_flow.cu", "k_track.cu", "k_klt.cu"]
+HEADERS = ["ft_internal.cuh", "ft_tracker.cuh", "ft_klt.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

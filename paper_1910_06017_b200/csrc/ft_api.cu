@@ -77,8 +77,6 @@ int check_flow_params(const ft_flow_params *p) {
   if (!(p->time_step > 0)) return fail(FT_EINVAL, "time_step must be positive");
   if (p->warps_per_level < 1) return fail(FT_EINVAL, "warps_per_level must be >= 1");
   if (p->iterations_per_warp < 1) return fail(FT_EINVAL, "iterations_per_warp must be >= 1");
-  if (p->pd_kernel != FT_PD_AUTO && p->pd_kernel != FT_PD_TILED)
-    return fail(FT_EINVAL, "pd_kernel must be FT_PD_AUTO or FT_PD_TILED");
   return FT_OK;
 }
 
@@ -316,7 +314,7 @@ int ft_compute_flow_traced(ft_ctx *ctx, const double *prev, const double *curr, 
   FT_TRY(build_flow_pyramid(curr, 0, geo, chain, p1, 0, 1, ctx->stream));
   FT_TRY(ctx->ensure_flow(1, (int64_t)w * h));
   FlowParamsD p{params->data_weight, params->time_step, params->huber_epsilon,
-                params->warps_per_level, params->iterations_per_warp, params->pd_kernel};
+                params->warps_per_level, params->iterations_per_warp};
   return run_flow(p0, p1, 0, geo.w.data(), geo.h.data(), geo.off.data(), scales, p, ctx->fw, dx,
                   dy, 0, 1, ctx->stream, d_energy_terms);
 }
@@ -334,7 +332,7 @@ int ft_flow_energy_terms(ft_ctx *ctx, const double *prev, const double *curr, co
   // flow_energy scales the frames by INTENSITY_SCALE first (optflow.py:143)
   FT_TRY(launch_scale_copy(prev, n, 0, i0, 0, 255.0, 1, ctx->stream));
   FT_TRY(launch_scale_copy(curr, n, 0, i1, 0, 255.0, 1, ctx->stream));
-  return launch_energy_terms(i0, i1, dx, dy, w, h, huber_epsilon, data, s1, s2, ctx->stream);
+  return launch_energy_terms(i0, i1, dx, dy, 1, w, h, huber_epsilon, data, s1, s2, ctx->stream);
 }
 
 static int check_boxes(const double *b, int n);
@@ -732,7 +730,7 @@ struct ft_tracker {
     // (3) feature calculation: TV-L1 between previous and current frame
     if (has_prev) {
       FlowParamsD p{cfg.flow.data_weight, cfg.flow.time_step, cfg.flow.huber_epsilon,
-                    cfg.flow.warps_per_level, cfg.flow.iterations_per_warp, cfg.flow.pd_kernel};
+                    cfg.flow.warps_per_level, cfg.flow.iterations_per_warp};
       FT_TRY(run_flow(pyr_prev, pyr_cur, geo.total, geo.w.data(), geo.h.data(),
                       geo.off.data(), scales, p, fw, d_dx, d_dy, P, S, s));
     }
@@ -1112,8 +1110,7 @@ int ft_tracker_profile_pd(ft_tracker *t, int reps, double *ms_per_launch, double
   FT_TRY(t->join_in());
   FT_CUDA_TRY(cudaStreamSynchronize(t->stream));
   FlowParamsD p{t->cfg.flow.data_weight, t->cfg.flow.time_step, t->cfg.flow.huber_epsilon,
-                t->cfg.flow.warps_per_level, t->cfg.flow.iterations_per_warp,
-                t->cfg.flow.pd_kernel};
+                t->cfg.flow.warps_per_level, t->cfg.flow.iterations_per_warp};
   int iters = 0;
   FT_TRY(profile_pd(t->fw, t->PW, t->PH, t->S, p, reps, t->stream, ms_per_launch, &iters));
   // algorithmic bytes of one launch per SURVEY.md 8(d): 152 B per

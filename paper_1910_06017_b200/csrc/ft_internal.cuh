@@ -163,22 +163,16 @@ struct FlowLevelPlanes {
   int64_t stride;
 };
 
-// Workspace for one batch of nb images at a max level size.
+// Workspace for one batch of nb images at a max level size (k_flow.cu
+// describes the interleaved double2 layout).
 struct FlowWork {
   int nb = 0;
-  int64_t cap = 0;  // elements per plane per image
-  // per-warp constants
-  double *gx = nullptr, *gy = nullptr, *r0 = nullptr;
-  // gradient of i1 (per level)
-  double *ix = nullptr, *iy = nullptr;
-  // primal-dual state, ping-pong (8 planes each: u1 u2 b1 b2 p11 p12 p21 p22)
-  double *st[2] = {nullptr, nullptr};
-  // whole-level primal-dual path (k_pd_level.cu): CTAs one cooperative
-  // launch holds on this device (0: unavailable), tile edge exchange records,
-  // half-step flags, timeout flag
-  int level_ctas = 0;
-  void *edges = nullptr;
-  unsigned *flags = nullptr, *err = nullptr;
+  int64_t cap = 0;  // pixels per plane per image
+  double2 *g = nullptr;   // (gx, gy) warp constants
+  double2 *rt = nullptr;  // (rho0, tau*lam*|grad|^2)
+  double2 *ix = nullptr;  // level gradient of I1
+  // primal-dual state ping-pong: [U | PX | PY][nb][cap] double2 each
+  double2 *st[2] = {nullptr, nullptr};
 };
 int flow_work_alloc(FlowWork &fw, int nb, int64_t cap);
 void flow_work_free(FlowWork &fw);
@@ -186,7 +180,6 @@ void flow_work_free(FlowWork &fw);
 struct FlowParamsD {
   double lam, tau, eps;
   int warps, iters;
-  int pd_kernel = FT_PD_AUTO;  // FT_PD_AUTO: whole-level kernel where a level fits; FT_PD_TILED
 };
 
 // Coarse-to-fine TV-L1 over nb image pairs given their (already scaled x255)
@@ -197,8 +190,9 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
              double *dx, double *dy, int64_t out_stride, int nb, cudaStream_t s,
              double *energy_terms = nullptr);
 
+// u1 / u2 element stride us (1: separate planes, 2: an interleaved U plane)
 int launch_energy_terms(const double *i0, const double *i1, const double *u1, const double *u2,
-                        int w, int h, double eps, double *data, double *s1, double *s2,
+                        int us, int w, int h, double eps, double *data, double *s1, double *s2,
                         cudaStream_t s);
 int profile_pd(FlowWork &fw, int w, int h, int nb, const FlowParamsD &p, int reps,
                cudaStream_t s, double *ms_per_launch, int *iters_per_launch);

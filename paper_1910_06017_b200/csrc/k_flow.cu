@@ -6,28 +6,31 @@
 // 3x3 median of both components (:210-211).  Between scales a bilinear
 // upsample scaled by the size ratio (:244-249).
 //
-// HBM layout (per batch of nb image pairs, all planes float64 row-major,
-// pitch == level width, capacity `cap` elements per plane):
-//   const planes  gx, gy, r0        [nb][cap]
-//   gradient      ix, iy            [nb][cap]
-//   state ping-pong st[2]           [8][nb][cap]  (u1 u2 b1 b2 p11 p12 p21 p22)
-// where b = "u bar" (optflow.py:173-174, :205-206).
+// HBM layout (per batch of nb image pairs, capacity `cap` pixels per stream
+// and plane, pitch == level width).  Fields used together are interleaved
+// as double2 so the tile kernel moves whole tiles with TMA box copies:
+//   U  (u1, u2)       state ping-pong st[2] = [U | PX | PY][nb][cap] double2
+//   PX (p11, p21)     (u-bar is recomputed at the start of every launch and
+//   PY (p12, p22)      never leaves the chip)
+//   G  (gx, gy)       warp constants          [nb][cap] double2
+//   RT (rho0, thresh)                         [nb][cap] double2
+//   IX (dI1/dx, dI1/dy) level gradient        [nb][cap] double2
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <type_traits>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "ft_internal.cuh"
-#include "ft_pd_level.cuh"
 
 namespace ft {
 
 namespace {
 
-enum { U1 = 0, U2, B1, B2, P11, P12, P21, P22, NST };
-
 struct StatePtrs {
-  double *p[NST];
+  double2 *u, *px, *py;
 };
 
 __device__ __forceinline__ double clip_lo_hi(double v, double lo, double hi) {
@@ -50,16 +53,27 @@ __device__ __forceinline__ double bsample(const double *__restrict__ img, int w,
   return top * (1.0 - fy) + bot * fy;
 }
 
+// the same sample of both components of an interleaved double2 plane (each
+// component in exactly bsample's operation order)
+__device__ __forceinline__ double2 bsample2(const double2 *__restrict__ img, int w, int h,
+                                            double x, double y) {
+  x = clip_lo_hi(x, 0.0, w - 1.0);
+  y = clip_lo_hi(y, 0.0, h - 1.0);
+  const int x0 = (int)floor(x), y0 = (int)floor(y);
+  const int x1 = min(x0 + 1, w - 1), y1 = min(y0 + 1, h - 1);
+  const double fx = x - (double)x0, fy = y - (double)y0;
+  const double2 *r0 = img + (int64_t)y0 * w;
+  const double2 *r1 = img + (int64_t)y1 * w;
+  const double2 a = r0[x0], b = r0[x1], c = r1[x0], d = r1[x1];
+  const double tx = a.x * (1.0 - fx) + b.x * fx, ty = a.y * (1.0 - fx) + b.y * fx;
+  const double bx = c.x * (1.0 - fx) + d.x * fx, by = c.y * (1.0 - fx) + d.y * fx;
+  return make_double2(tx * (1.0 - fy) + bx * fy, ty * (1.0 - fy) + by * fy);
+}
+
 // np.gradient(i1) with unit spacing (optflow.py:155): central inside,
 // one-sided at the borders.  (a-b)/2 == (a-b)*0.5 exactly.
-__global__ void k_central_grad(const double *__restrict__ img, int w, int h, int64_t is,
-                               double *__restrict__ gx, double *__restrict__ gy, int64_t gs) {
-  img += blockIdx.z * is;
-  gx += blockIdx.z * gs;
-  gy += blockIdx.z * gs;
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  const int r = blockIdx.y * blockDim.y + threadIdx.y;
-  if (r >= h || c >= w) return;
+__device__ __forceinline__ double2 central_grad_at(const double *__restrict__ img, int w, int h,
+                                                   int c, int r) {
   const int64_t o = (int64_t)r * w + c;
   double vx, vy;
   if (c == 0)
@@ -74,39 +88,58 @@ __global__ void k_central_grad(const double *__restrict__ img, int w, int h, int
     vy = img[o] - img[o - w];
   else
     vy = (img[o + w] - img[o - w]) * 0.5;
-  gx[o] = vx;
-  gy[o] = vy;
+  return make_double2(vx, vy);
+}
+
+// separate gx / gy planes (the KLT backend's pyramids)
+__global__ void k_central_grad(const double *__restrict__ img, int w, int h, int64_t is,
+                               double *__restrict__ gx, double *__restrict__ gy, int64_t gs) {
+  img += blockIdx.z * is;
+  gx += blockIdx.z * gs;
+  gy += blockIdx.z * gs;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = blockIdx.y * blockDim.y + threadIdx.y;
+  if (r >= h || c >= w) return;
+  const double2 g = central_grad_at(img, w, h, c, r);
+  const int64_t o = (int64_t)r * w + c;
+  gx[o] = g.x;
+  gy[o] = g.y;
+}
+
+// interleaved IX plane (the flow's warp setup gathers both with one sample)
+__global__ void k_central_grad2(const double *__restrict__ img, int w, int h, int64_t is,
+                                double2 *__restrict__ ix, int64_t cap) {
+  img += blockIdx.z * is;
+  ix += blockIdx.z * cap;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = blockIdx.y * blockDim.y + threadIdx.y;
+  if (r >= h || c >= w) return;
+  ix[(int64_t)r * w + c] = central_grad_at(img, w, h, c, r);
 }
 
 // resize_bilinear(u, w, h) * ratio for both components (optflow.py:244-249,
 // imageops.py:69-75).  rx = wc/wf, ry = hc/hf (host-computed IEEE quotients),
 // sx = wf/wc, sy = hf/hc.
-__global__ void k_upsample(const double *__restrict__ cu1, const double *__restrict__ cu2,
-                           int wc, int hc, double *__restrict__ fu1, double *__restrict__ fu2,
-                           int wf, int hf, int64_t cap, double rx, double ry, double sx,
-                           double sy) {
-  cu1 += blockIdx.z * cap;
-  cu2 += blockIdx.z * cap;
-  fu1 += blockIdx.z * cap;
-  fu2 += blockIdx.z * cap;
+__global__ void k_upsample(const double2 *__restrict__ cu, int wc, int hc,
+                           double2 *__restrict__ fu, int wf, int hf, int64_t cap, double rx,
+                           double ry, double sx, double sy) {
+  cu += blockIdx.z * cap;
+  fu += blockIdx.z * cap;
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int r = blockIdx.y * blockDim.y + threadIdx.y;
   if (r >= hf || c >= wf) return;
   const double x = ((double)c + 0.5) * rx - 0.5;
   const double y = ((double)r + 0.5) * ry - 0.5;
-  const int64_t o = (int64_t)r * wf + c;
-  fu1[o] = bsample(cu1, wc, hc, x, y) * sx;
-  fu2[o] = bsample(cu2, wc, hc, x, y) * sy;
+  const double2 v = bsample2(cu, wc, hc, x, y);
+  fu[(int64_t)r * wf + c] = make_double2(v.x * sx, v.y * sy);
 }
 
-// Per-warp linearisation (optflow.py:158-167): gather I1, dI1/dx, dI1/dy at
-// x+u; rho0 = I1w - I0 - gx*u1 - gy*u2.
+// Per-warp linearisation (optflow.py:158-176): gather I1, dI1/dx, dI1/dy at
+// x+u; rho0 = I1w - I0 - gx*u1 - gy*u2; thresh = tau*lam*|grad|^2.
 __global__ void k_warp_setup(const double *__restrict__ i0, const double *__restrict__ i1,
-                             int64_t ps, const double *__restrict__ ix,
-                             const double *__restrict__ iy, const double *__restrict__ u1,
-                             const double *__restrict__ u2, int w, int h, int64_t cap,
-                             double *__restrict__ gx, double *__restrict__ gy,
-                             double *__restrict__ r0) {
+                             int64_t ps, const double2 *__restrict__ ix,
+                             const double2 *__restrict__ u, int w, int h, int64_t cap, double tl,
+                             double2 *__restrict__ g, double2 *__restrict__ rt) {
   i0 += blockIdx.z * ps;
   i1 += blockIdx.z * ps;
   const int64_t so = blockIdx.z * cap;
@@ -114,14 +147,13 @@ __global__ void k_warp_setup(const double *__restrict__ i0, const double *__rest
   const int r = blockIdx.y * blockDim.y + threadIdx.y;
   if (r >= h || c >= w) return;
   const int64_t o = (int64_t)r * w + c;
-  const double a = u1[so + o], b = u2[so + o];
-  const double mx = (double)c + a, my = (double)r + b;
+  const double2 uu = u[so + o];
+  const double mx = (double)c + uu.x, my = (double)r + uu.y;
   const double v = bsample(i1, w, h, mx, my);
-  const double g1 = bsample(ix + so, w, h, mx, my);
-  const double g2 = bsample(iy + so, w, h, mx, my);
-  gx[so + o] = g1;
-  gy[so + o] = g2;
-  r0[so + o] = v - i0[o] - g1 * a - g2 * b;
+  const double2 gg = bsample2(ix + so, w, h, mx, my);
+  g[so + o] = gg;
+  const double g2 = gg.x * gg.x + gg.y * gg.y;  // optflow.py:163
+  rt[so + o] = make_double2(v - i0[o] - gg.x * uu.x - gg.y * uu.y, tl * g2);
 }
 
 // 3x3 median with replicated border (imageops.py:78-84): exact 5th order
@@ -132,18 +164,6 @@ __device__ __forceinline__ void cswap(double &a, double &b) {
   b = hi;
 }
 
-__device__ __forceinline__ double median9(double *v) {
-  // Paeth / Devillard opt_med9 network (19 compare-swaps)
-  cswap(v[1], v[2]); cswap(v[4], v[5]); cswap(v[7], v[8]);
-  cswap(v[0], v[1]); cswap(v[3], v[4]); cswap(v[6], v[7]);
-  cswap(v[1], v[2]); cswap(v[4], v[5]); cswap(v[7], v[8]);
-  cswap(v[0], v[3]); cswap(v[5], v[8]); cswap(v[4], v[7]);
-  cswap(v[3], v[6]); cswap(v[1], v[4]); cswap(v[2], v[5]);
-  cswap(v[4], v[7]); cswap(v[4], v[2]); cswap(v[6], v[4]);
-  cswap(v[4], v[2]);
-  return v[4];
-}
-
 __device__ __forceinline__ double med3(double a, double b, double c) {
   return fmax(fmin(a, b), fmin(fmax(a, b), c));
 }
@@ -151,9 +171,8 @@ __device__ __forceinline__ double med3(double a, double b, double c) {
 // Two horizontally adjacent outputs per thread: the four 3-sample columns
 // c-1..c+2 are sorted once and shared; median9 = med3(max of the column
 // minima, med3 of the column medians, min of the column maxima), the same
-// order statistic as the sort (exact selection).
-__global__ void k_median(const double *__restrict__ a1, const double *__restrict__ a2,
-                         double *__restrict__ o1, double *__restrict__ o2, int w, int h,
+// order statistic as the sort (exact selection).  Both components of U.
+__global__ void k_median(const double2 *__restrict__ in, double2 *__restrict__ out, int w, int h,
                          int64_t cap) {
   const int64_t so = blockIdx.z * cap;
   const int c = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
@@ -164,58 +183,78 @@ __global__ void k_median(const double *__restrict__ a1, const double *__restrict
 #pragma unroll
   for (int k = 0; k < 4; ++k) cc[k] = min(max(c - 1 + k, 0), w - 1);
   const bool two = c + 1 < w;
+  const double2 *a = in + so;
+  double lo[2][4], md[2][4], hi[2][4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double2 x = a[rr[0] + cc[k]], y = a[rr[1] + cc[k]], z = a[rr[2] + cc[k]];
+    double x0 = x.x, y0 = y.x, z0 = z.x, x1 = x.y, y1 = y.y, z1 = z.y;
+    cswap(x0, y0);
+    cswap(y0, z0);
+    cswap(x0, y0);
+    cswap(x1, y1);
+    cswap(y1, z1);
+    cswap(x1, y1);
+    lo[0][k] = x0, md[0][k] = y0, hi[0][k] = z0;
+    lo[1][k] = x1, md[1][k] = y1, hi[1][k] = z1;
+  }
+  double m[2][2];
 #pragma unroll
   for (int f = 0; f < 2; ++f) {
-    const double *a = (f ? a2 : a1) + so;
-    double lo[4], md[4], hi[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      double x = a[rr[0] + cc[k]], y = a[rr[1] + cc[k]], z = a[rr[2] + cc[k]];
-      cswap(x, y);
-      cswap(y, z);
-      cswap(x, y);
-      lo[k] = x, md[k] = y, hi[k] = z;
-    }
-    double *o = (f ? o2 : o1) + so + (int64_t)r * w + c;
-    o[0] = med3(fmax(fmax(lo[0], lo[1]), lo[2]), med3(md[0], md[1], md[2]),
-                fmin(fmin(hi[0], hi[1]), hi[2]));
-    if (two)
-      o[1] = med3(fmax(fmax(lo[1], lo[2]), lo[3]), med3(md[1], md[2], md[3]),
-                  fmin(fmin(hi[1], hi[2]), hi[3]));
+    m[f][0] = med3(fmax(fmax(lo[f][0], lo[f][1]), lo[f][2]), med3(md[f][0], md[f][1], md[f][2]),
+                   fmin(fmin(hi[f][0], hi[f][1]), hi[f][2]));
+    m[f][1] = med3(fmax(fmax(lo[f][1], lo[f][2]), lo[f][3]), med3(md[f][1], md[f][2], md[f][3]),
+                   fmin(fmin(hi[f][1], hi[f][2]), hi[f][3]));
   }
+  double2 *o = out + so + (int64_t)r * w + c;
+  o[0] = make_double2(m[0][0], m[1][0]);
+  if (two) o[1] = make_double2(m[0][1], m[1][1]);
 }
 
 // Per-pixel terms of the TV-L1 objective (optflow.py:121-137): data term
 // |I1(x+u) - I0| and, per component, huber(hypot(forward_gradient(u))).
 // The reference sums these arrays with numpy; the caller does exactly that
-// on the host copies, so the scalar is bit-identical too.
+// on the host copies, so the scalar is bit-identical too.  u1/u2 element
+// stride us: 1 for separate planes, 2 for an interleaved U plane.
 __global__ void k_energy_terms(const double *__restrict__ i0, const double *__restrict__ i1,
                                const double *__restrict__ u1, const double *__restrict__ u2,
-                               int w, int h, double eps, double *__restrict__ data,
+                               int us, int w, int h, double eps, double *__restrict__ data,
                                double *__restrict__ s1, double *__restrict__ s2) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int r = blockIdx.y * blockDim.y + threadIdx.y;
   if (r >= h || c >= w) return;
   const int64_t o = (int64_t)r * w + c;
-  const double v = bsample(i1, w, h, (double)c + u1[o], (double)r + u2[o]);
+  const double v = bsample(i1, w, h, (double)c + u1[us * o], (double)r + u2[us * o]);
   data[o] = fabs(v - i0[o]);
   const double *comp[2] = {u1, u2};
   double *dst[2] = {s1, s2};
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
     const double *u = comp[k];
-    const double gx = c < w - 1 ? u[o + 1] - u[o] : 0.0;
-    const double gy = r < h - 1 ? u[o + w] - u[o] : 0.0;
+    const double gx = c < w - 1 ? u[us * (o + 1)] - u[us * o] : 0.0;
+    const double gy = r < h - 1 ? u[us * (o + w)] - u[us * o] : 0.0;
     const double m = glibc_hypot(gx, gy);
     // _huber (optflow.py:121-124)
     dst[k][o] = eps <= 0.0 ? m : (m <= eps ? m * m / (2.0 * eps) : m - eps / 2.0);
   }
 }
 
-StatePtrs state_ptrs(double *base, int nb, int64_t cap) {
-  StatePtrs s;
-  for (int k = 0; k < NST; ++k) s.p[k] = base + (int64_t)k * nb * cap;
-  return s;
+// the finest level's U -> the caller's dx / dy planes
+__global__ void k_split(const double2 *__restrict__ u, int64_t n, int64_t cap,
+                        double *__restrict__ dx, double *__restrict__ dy, int64_t os) {
+  u += blockIdx.z * cap;
+  dx += blockIdx.z * os;
+  dy += blockIdx.z * os;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 v = u[i];
+    dx[i] = v.x;
+    dy[i] = v.y;
+  }
+}
+
+StatePtrs state_ptrs(double2 *base, int nb, int64_t cap) {
+  return StatePtrs{base, base + (int64_t)nb * cap, base + 2 * (int64_t)nb * cap};
 }
 
 // ------------------------------------------------------------------------
@@ -238,11 +277,15 @@ StatePtrs state_ptrs(double *base, int nb, int64_t cap) {
 // launch) live in registers of the owning thread: thread (tx, ty) owns
 // columns tx + 32*cx (cx < TW/32) and rows ty + BY*k (k < PY).
 // ------------------------------------------------------------------------
-struct PDArgs {
-  StatePtrs in, out;
-  const double *gx, *gy, *r0;
+struct alignas(64) PDArgs {
+  // TMA descriptors (3-D: interleaved row, y, image of the batch), built per
+  // launch: the tile plus its one-element apron of U / PX / PY, the tile's
+  // G / RT, and the written interior of U / PX / PY.  Boxes that stick out
+  // of the image are zero-filled on load and clipped on store.
+  CUtensorMap in_u, in_px, in_py;
+  CUtensorMap in_g, in_rt;
+  CUtensorMap out_u, out_px, out_py;
   int w, h;
-  int64_t cap;
   int halo, first, nb;
   int pow2;  // sigma and tau are powers of two (exact fused multiply-adds)
   // k_pd_tile half-step schedule: the launch runs `nhalf` alternating dual (D)
@@ -256,7 +299,7 @@ struct PDArgs {
 };
 
 // per-pixel border flags (global position, fixed for the launch)
-enum : unsigned { FL_R = 1, FL_D = 2, FL_L = 4, FL_LASTC = 8, FL_U = 16, FL_LASTR = 32, FL_OK = 64 };
+enum : unsigned { FL_R = 1, FL_D = 2, FL_L = 4, FL_LASTC = 8, FL_U = 16, FL_LASTR = 32 };
 
 // Exchange planes hold the fields read at a neighbour as three interleaved
 // double2 planes -- (b1,b2), (p11,p21), (p12,p22) -- the pairs that are always
@@ -272,11 +315,65 @@ __device__ __forceinline__ int sxi(int f, int id, int PL) {
 template <int TW, int BY, int PY>
 struct PDGeom {
   static constexpr int NX = TW / 32, TH = BY * PY, NP = NX * PY;
-  static constexpr int SP = TW + 2, SR = TH + 2, PLANE = SP * SR;
-  // 6 exchange planes + the CTA-wide projection queue (one int per pair,
-  // 2*NP pairs per thread) and its two counters
-  static constexpr size_t smem = 6 * PLANE * sizeof(double) + (2 * NP * 32 * BY + 2) * sizeof(int);
+  static constexpr int SP = TW + 2, SR = TH + 2;
+  // plane stride in double2, rounded to 128 bytes (TMA destinations)
+  static constexpr int PLANE = (SP * SR + 7) / 8 * 8;
+  // shared memory: 3 exchange planes | staging (in: G and RT boxes of the
+  // tile; out: the U / PX / PY interior boxes) | CTA projection queue (one
+  // int per pair, 2*NP pairs per thread, two counters) | mbarrier
+  static constexpr size_t kPlanes = (size_t)3 * PLANE * 16;
+  static constexpr size_t kStage = (size_t)2 * TW * TH * 16;
+  static constexpr size_t kQueue = ((size_t)(2 * NP * 32 * BY + 2) * 4 + 15) / 16 * 16;
+  static constexpr size_t smem = kPlanes + kStage + kQueue + 16;
 };
+
+// ---- TMA / mbarrier primitives (PTX)
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "FT_MBAR_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra FT_MBAR_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// box at pixel (x, y) of image z of a plane_map (x counts double2 pixels)
+__device__ __forceinline__ void tma_load(void *dst, const CUtensorMap *m, int x, int y, int z,
+                                         uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(2 * x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store(const CUtensorMap *m, int x, int y, int z,
+                                          const void *src) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+          reinterpret_cast<uint64_t>(m)),
+      "r"(2 * x), "r"(y), "r"(z), "r"(smem_u32(src))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_commit_wait() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+// generic-proxy shared-memory writes -> visible to the async (TMA) proxy
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 
 // a*b + c.  With P2 the product is exact (b or a is a power of two: sigma
 // and tau for the default time_step 0.25, the literal 2.0), so one fused
@@ -443,102 +540,86 @@ __device__ __forceinline__ void pd_halfsteps_cq(const PDArgs &a, double *sm, int
   }
 }
 
-// global -> shared copies without register staging (LDGSTS)
-__device__ __forceinline__ void cp_async8(double *dst, const double *src, bool valid) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  const int n = valid ? 8 : 0;  // src-size 0: zero-fill the 8 bytes
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(n));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-}
-
+// Tile movement is TMA: one elected thread issues box copies of the tile
+// (+ apron) of U / PX / PY and of the tile's G / RT straight into shared
+// memory, completing on an mbarrier, and stores the written interior of U /
+// PX / PY with TMA box stores from a shared staging area.  Out-of-image
+// elements are zero-filled on load (the reference's zeros outside the
+// image never reach an interior pixel) and clipped on store.
 template <int TW, int BY, int PY, int MINB, bool MID = false>
-__global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const PDArgs a) {
+__global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const __grid_constant__ PDArgs a) {
   using G = PDGeom<TW, BY, PY>;
-  constexpr int NX = G::NX, TH = G::TH, NP = G::NP, SP = G::SP, PL = G::PLANE;
-  extern __shared__ __align__(16) double sm[];
+  constexpr int NX = G::NX, TH = G::TH, NP = G::NP, SP = G::SP, SR = G::SR, PL = G::PLANE;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  double *const sm = reinterpret_cast<double *>(smraw);
+  double2 *const sB = reinterpret_cast<double2 *>(smraw);
+  double2 *const stage = reinterpret_cast<double2 *>(smraw + G::kPlanes);
+  int *const qidx = reinterpret_cast<int *>(smraw + G::kPlanes + G::kStage);
+  int *const ctr = qidx + 2 * NP * 32 * BY;
+  uint64_t *const bar = reinterpret_cast<uint64_t *>(smraw + G::kPlanes + G::kStage + G::kQueue);
 
   const int W = a.w, H = a.h;
   const int step_x = TW - 2 * a.halo, step_y = TH - 2 * a.halo;
   const int ox = (int)blockIdx.x * step_x - a.halo;
   const int oy = blockIdx.y * step_y - a.halo;
-  const int64_t so = blockIdx.z * a.cap;
+  const int bz = blockIdx.z;
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = ty * 32 + tx;
   const int base = (ty + 1) * SP + tx + 1;  // apron offset (+1,+1)
 
-  // zero the apron ring once (read only by halo pixels, keeps them finite)
-  for (int k = tid; k < 2 * SP + 2 * TH; k += 32 * BY) {
-    int idx;
-    if (k < SP) idx = k;
-    else if (k < 2 * SP) idx = (TH + 1) * SP + (k - SP);
-    else if (k < 2 * SP + TH) idx = (k - 2 * SP + 1) * SP;
-    else idx = (k - 2 * SP - TH + 1) * SP + SP - 1;
-#pragma unroll
-    for (int f = 0; f < 6; ++f) sm[sxi(f, idx, PL)] = 0.0;
+  // ---- prologue: U (-> u-bar plane: u-bar = u), p, G, RT by TMA
+  if (tid == 0) mbar_init(bar, 1);
+  __syncthreads();
+  if (tid == 0) {
+    const unsigned box = SP * SR * 16, own = TW * TH * 16;
+    mbar_expect_tx(bar, box * (a.first ? 1 : 3) + 2 * own);
+    tma_load(sB, &a.in_u, ox - 1, oy - 1, bz, bar);
+    if (!a.first) {
+      tma_load(sB + PL, &a.in_px, ox - 1, oy - 1, bz, bar);
+      tma_load(sB + 2 * PL, &a.in_py, ox - 1, oy - 1, bz, bar);
+    }
+    tma_load(stage, &a.in_g, ox, oy, bz, bar);
+    tma_load(stage + TW * TH, &a.in_rt, ox, oy, bz, bar);
   }
+  if (a.first) {  // p = 0 at the start of a warp (optflow.py:169-172)
+    for (int k = tid; k < SP * SR; k += 32 * BY) {
+      sB[PL + k] = make_double2(0.0, 0.0);
+      sB[2 * PL + k] = make_double2(0.0, 0.0);
+    }
+  }
+  if (tid < 2) ctr[tid] = 0;
+  mbar_wait(bar, 0);
 
   const double tl = a.tau * a.lam;
   double u1[NP], u2[NP], gx[NP], gy[NP], r0[NP], thr[NP], ig2[NP];
   unsigned fl[NP];
-
 #pragma unroll
   for (int k = 0; k < PY; ++k) {
 #pragma unroll
     for (int cx = 0; cx < NX; ++cx) {
       const int q = k * NX + cx;
-      const int gc = ox + tx + 32 * cx, gr = oy + ty + BY * k;
-      const bool in = gc >= 0 && gc < W && gr >= 0 && gr < H;
-      const int64_t o = so + (int64_t)gr * W + gc;
-      const int id = base + k * BY * SP + 32 * cx;
-      // p planes go straight to shared memory (cp.async, zero-filled outside
-      // the image): no registers held, all copies in flight at once.  u-bar
-      // is not part of the state between launches: the launch opens with a
-      // primal half-step that writes it (first launch: u-bar = u, p = 0).
-      if (!a.first) {
-#pragma unroll
-        for (int f = 2; f < 6; ++f)
-          cp_async8(&sm[sxi(f, id, PL)], in ? a.in.p[B1 + f] + o : a.in.p[B1 + f], in);
-      }
-      double vu1 = 0, vu2 = 0, vgx = 0, vgy = 0, vr0 = 0;
-      if (in) {
-        vu1 = a.in.p[U1][o];
-        vu2 = a.in.p[U2][o];
-        vgx = a.gx[o];
-        vgy = a.gy[o];
-        vr0 = a.r0[o];
-      }
-      u1[q] = vu1;
-      u2[q] = vu2;
-      gx[q] = vgx;
-      gy[q] = vgy;
-      r0[q] = vr0;
-      const double g2 = vgx * vgx + vgy * vgy;  // optflow.py:163
-      const bool ok = g2 > 1e-12;
-      ig2[q] = ok ? 1.0 / (g2 > 1e-12 ? g2 : 1e-12) : 0.0;
-      thr[q] = tl * g2;  // tau*lam*grad_sq (optflow.py:176)
+      const int lc = tx + 32 * cx, lr = ty + BY * k;
+      const int gc = ox + lc, gr = oy + lr;
+      const double2 u = sB[base + k * BY * SP + 32 * cx];
+      const double2 g = stage[lr * TW + lc];
+      const double2 rt = stage[TW * TH + lr * TW + lc];
+      u1[q] = u.x;
+      u2[q] = u.y;
+      gx[q] = g.x;
+      gy[q] = g.y;
+      r0[q] = rt.x;
+      thr[q] = rt.y;  // tau*lam*grad_sq (optflow.py:176), from the warp setup
+      const double g2 = g.x * g.x + g.y * g.y;  // optflow.py:163-165
+      ig2[q] = g2 > 1e-12 ? 1.0 / g2 : 0.0;
       fl[q] = (gc < W - 1 ? FL_R : 0u) | (gr < H - 1 ? FL_D : 0u) | (gc > 0 ? FL_L : 0u) |
-              (gc == W - 1 ? FL_LASTC : 0u) | (gr > 0 ? FL_U : 0u) | (gr == H - 1 ? FL_LASTR : 0u) |
-              (ok ? FL_OK : 0u);
-      if (a.first) {  // ub = u, p = 0 at the start of a warp (optflow.py:169-174)
-        sm[sxi(0, id, PL)] = vu1;
-        sm[sxi(1, id, PL)] = vu2;
-#pragma unroll
-        for (int f = 2; f < 6; ++f) sm[sxi(f, id, PL)] = 0.0;
-      }
+              (gc == W - 1 ? FL_LASTC : 0u) | (gr > 0 ? FL_U : 0u) | (gr == H - 1 ? FL_LASTR : 0u);
     }
   }
-  if (!a.first) cp_async_wait_all();
-  if (tid < 2) reinterpret_cast<int *>(sm + 6 * PL)[2 * NP * 32 * BY + tid] = 0;  // queue counters
   __syncthreads();
 
   // tile free of image-border pixels (uniform per CTA): flag-free fast path
   const bool interior = ox >= 1 && oy >= 1 && ox + TW <= W - 1 && oy + TH <= H - 1;
   {
-    int *const qidx = reinterpret_cast<int *>(sm + 6 * PL);
-    int *const ctr = qidx + 2 * NP * 32 * BY;
 #define FT_PD_CALL(P2_, IN_)                                                                 \
   pd_halfsteps_cq<TW, BY, PY, P2_, IN_, MID>(a, sm, base, tx, ty, fl, u1, u2, gx, gy, r0, thr, ig2, \
                                         tl, qidx, ctr)
@@ -550,25 +631,33 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const PDArgs a) {
 #undef FT_PD_CALL
   }
 
-  // ---- write back the exact interior: u, and p unless this is the warp's
-  // last launch (the next warp starts from p = 0)
-  const int lo_x = a.halo, hi_x = TW - a.halo;
-  const int lo_y = a.halo, hi_y = TH - a.halo;
+  // ---- epilogue: the exact interior of u, and of p unless this is the
+  // warp's last launch (the next warp starts from p = 0), staged densely and
+  // stored by TMA (the G / RT staging is dead by now)
+  const int hl = a.halo, iw = TW - 2 * hl, ih = TH - 2 * hl;
+  double2 *const ou = stage, *const opx = stage + iw * ih, *const opy = stage + 2 * iw * ih;
 #pragma unroll
   for (int q = 0; q < NP; ++q) {
     const int k = q / NX, cx = q % NX;
     const int lc = tx + 32 * cx, lr = ty + BY * k;
-    const int gc = ox + lc, gr = oy + lr;
-    if (gc < 0 || gc >= W || gr < 0 || gr >= H) continue;
-    if (lc < lo_x || lc >= hi_x || lr < lo_y || lr >= hi_y) continue;
-    const int id = base + k * BY * SP + 32 * cx;
-    const int64_t o = so + (int64_t)gr * W + gc;
-    a.out.p[U1][o] = u1[q];
-    a.out.p[U2][o] = u2[q];
+    if (lc < hl || lc >= TW - hl || lr < hl || lr >= TH - hl) continue;
+    const int e = (lr - hl) * iw + (lc - hl);
+    ou[e] = make_double2(u1[q], u2[q]);
     if (!a.last) {
-#pragma unroll
-      for (int f = 2; f < 6; ++f) a.out.p[B1 + f][o] = sm[sxi(f, id, PL)];
+      const int id = base + k * BY * SP + 32 * cx;
+      opx[e] = sB[PL + id];
+      opy[e] = sB[2 * PL + id];
     }
+  }
+  fence_proxy_async();
+  __syncthreads();
+  if (tid == 0) {
+    tma_store(&a.out_u, ox + hl, oy + hl, bz, ou);
+    if (!a.last) {
+      tma_store(&a.out_px, ox + hl, oy + hl, bz, opx);
+      tma_store(&a.out_py, ox + hl, oy + hl, bz, opy);
+    }
+    tma_store_commit_wait();
   }
 }
 
@@ -577,7 +666,7 @@ struct PDConfig {
   int tw, th, by;
   void (*fn)(PDArgs);
   void (*fn_mid)(PDArgs);  // k_pd_tile<..., MID>: middle (P D)x4 launches, halo 4
-  size_t smem;             // six exchange planes + the CTA-wide projection queue
+  size_t smem;             // exchange planes, TMA staging, projection queue, mbarrier
 };
 
 template <int TW, int BY, int PY, int MINB>
@@ -587,12 +676,59 @@ PDConfig make_cfg() {
                   G::TH == 32 ? &k_pd_tile<TW, BY, PY, MINB, G::TH == 32> : nullptr, G::smem};
 }
 
-// The launch sets the shared-memory limit on every call: the attribute is
-// per device context, and a process may run trackers on several GPUs.
-int pd_launch(const PDConfig &c, const PDArgs &a, int nb, cudaStream_t s) {
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no
+// link-time dependency on libcuda)
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+// 3-D map over nb interleaved double2 planes of w x h (stream stride cap
+// pixels), viewed as rows of 2w doubles so a box row is one contiguous run
+// of 2*bw doubles (a 16-byte innermost box dimension starves the TMA unit):
+// dims (2w, h, image), box (2*bw, bh, 1)
+int plane_map(CUtensorMap *m, const double2 *base, int w, int h, int nb, int64_t cap, int bw,
+              int bh) {
+  PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+  if (!enc) return fail(FT_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[3] = {2 * (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)nb};
+  const cuuint64_t strides[2] = {(cuuint64_t)w * 16, (cuuint64_t)cap * 16};
+  const cuuint32_t box[3] = {2 * (cuuint32_t)bw, (cuuint32_t)bh, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double2 *>(base), dims,
+                         strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(FT_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return FT_OK;
+}
+
+// Builds the launch's TMA maps and launches.  The shared-memory limit is set
+// on every call: the attribute is per device context, and a process may run
+// trackers on several GPUs.
+int pd_launch(const PDConfig &c, PDArgs &a, const StatePtrs &in, const StatePtrs &out,
+              const double2 *g, const double2 *rt, int64_t cap, int nb, cudaStream_t s) {
   const int step_x = c.tw - 2 * a.halo, step_y = c.th - 2 * a.halo;
   const dim3 grid(a.halo ? (a.w + step_x - 1) / step_x : 1, a.halo ? (a.h + step_y - 1) / step_y : 1,
                   nb);
+  const int bw = c.tw + 2, bh = c.th + 2, iw = step_x, ih = step_y;
+  FT_TRY(plane_map(&a.in_u, in.u, a.w, a.h, nb, cap, bw, bh));
+  FT_TRY(plane_map(&a.in_px, in.px, a.w, a.h, nb, cap, bw, bh));
+  FT_TRY(plane_map(&a.in_py, in.py, a.w, a.h, nb, cap, bw, bh));
+  FT_TRY(plane_map(&a.in_g, g, a.w, a.h, nb, cap, c.tw, c.th));
+  FT_TRY(plane_map(&a.in_rt, rt, a.w, a.h, nb, cap, c.tw, c.th));
+  FT_TRY(plane_map(&a.out_u, out.u, a.w, a.h, nb, cap, iw, ih));
+  FT_TRY(plane_map(&a.out_px, out.px, a.w, a.h, nb, cap, iw, ih));
+  FT_TRY(plane_map(&a.out_py, out.py, a.w, a.h, nb, cap, iw, ih));
   const bool mid = c.fn_mid && !a.first && !a.last && a.nhalf == 8 && a.halo == 4 && a.cone_rows &&
                    c.th == 32;
   void (*fn)(PDArgs) = mid ? c.fn_mid : c.fn;
@@ -685,12 +821,8 @@ int profile_pd(FlowWork &fw, int w, int h, int nb, const FlowParamsD &p, int rep
   const int halo = plan.halo;
   const int iters = halo ? std::min(halo, p.iters) : p.iters;
   PDArgs a;
-  a.gx = fw.gx;
-  a.gy = fw.gy;
-  a.r0 = fw.r0;
   a.w = w;
   a.h = h;
-  a.cap = fw.cap;
   a.halo = halo;
   a.nb = nb;
   a.pow2 = pow2_params(p.tau);
@@ -708,9 +840,8 @@ int profile_pd(FlowWork &fw, int w, int h, int nb, const FlowParamsD &p, int rep
   // one untimed launch to warm the instruction cache
   for (int r = -1; r < reps; ++r) {
     if (r == 0) FT_CUDA_TRY(cudaEventRecord(e0, s));
-    a.in = state_ptrs(fw.st[cur], fw.nb, fw.cap);
-    a.out = state_ptrs(fw.st[1 - cur], fw.nb, fw.cap);
-    FT_TRY(pd_launch(plan.cfg, a, nb, s));
+    FT_TRY(pd_launch(plan.cfg, a, state_ptrs(fw.st[cur], fw.nb, fw.cap),
+                     state_ptrs(fw.st[1 - cur], fw.nb, fw.cap), fw.g, fw.rt, fw.cap, nb, s));
     cur = 1 - cur;
   }
   FT_CUDA_TRY(cudaEventRecord(e1, s));
@@ -729,40 +860,22 @@ int flow_work_alloc(FlowWork &fw, int nb, int64_t cap) {
   flow_work_free(fw);
   fw.nb = nb;
   fw.cap = cap;
-  const size_t plane = (size_t)nb * cap * sizeof(double);
-  double *all = nullptr;
-  // gx gy r0 ix iy + 2 x 8 state planes
-  cudaError_t e = cudaMalloc(&all, plane * (5 + 2 * NST));
+  const size_t plane = (size_t)nb * cap * sizeof(double2);
+  double2 *all = nullptr;
+  // G RT IX + 2 x (U PX PY)
+  cudaError_t e = cudaMalloc(&all, plane * 9);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(flow workspace)");
   const int64_t pe = (int64_t)nb * cap;
-  fw.gx = all;
-  fw.gy = all + pe;
-  fw.r0 = all + 2 * pe;
-  fw.ix = all + 3 * pe;
-  fw.iy = all + 4 * pe;
-  fw.st[0] = all + 5 * pe;
-  fw.st[1] = all + (5 + NST) * pe;
-  // whole-level primal-dual path: exchange records + flags for the CTAs one
-  // cooperative launch holds on this device
-  int dev = 0;
-  FT_CUDA_TRY(cudaGetDevice(&dev));
-  FT_TRY(level_pd_capacity(dev, &fw.level_ctas));
-  if (fw.level_ctas > 0) {
-    const size_t eb = level_pd_edges_bytes(fw.level_ctas);
-    char *x = nullptr;
-    e = cudaMalloc(&x, eb + (size_t)(2 * fw.level_ctas + 64) * sizeof(unsigned));
-    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(level exchange)");
-    fw.edges = x;
-    fw.flags = reinterpret_cast<unsigned *>(x + eb);
-    fw.err = fw.flags + 2 * fw.level_ctas;
-    FT_CUDA_TRY(cudaMemset(fw.err, 0, sizeof(unsigned)));
-  }
+  fw.g = all;
+  fw.rt = all + pe;
+  fw.ix = all + 2 * pe;
+  fw.st[0] = all + 3 * pe;
+  fw.st[1] = all + 6 * pe;
   return FT_OK;
 }
 
 void flow_work_free(FlowWork &fw) {
-  if (fw.gx) cudaFree(fw.gx);
-  if (fw.edges) cudaFree(fw.edges);
+  if (fw.g) cudaFree(fw.g);
   fw = FlowWork();
 }
 
@@ -775,84 +888,47 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
   int cur = 0;
   const double sigma = 1.0 / (8.0 * p.tau);
   const double shrink = 1.0 / (1.0 + sigma * p.eps);
+  const double tl = p.tau * p.lam;
   const dim3 blk(32, 8);
   for (int lvl = scales - 1; lvl >= 0; --lvl) {
     const int w = lw[lvl], h = lh[lvl];
-    StatePtrs st = state_ptrs(fw.st[cur], fw.nb, cap);
     if (lvl == scales - 1) {  // zero flow at the coarsest scale (optflow.py:239-240)
-      for (int b = 0; b < nb; ++b) {
-        FT_CUDA_TRY(cudaMemsetAsync(st.p[U1] + b * cap, 0, (size_t)w * h * 8, s));
-        FT_CUDA_TRY(cudaMemsetAsync(st.p[U2] + b * cap, 0, (size_t)w * h * 8, s));
-      }
+      const StatePtrs st = state_ptrs(fw.st[cur], fw.nb, cap);
+      for (int b = 0; b < nb; ++b)
+        FT_CUDA_TRY(cudaMemsetAsync(st.u + b * cap, 0, (size_t)w * h * sizeof(double2), s));
     } else {
       const int wc = lw[lvl + 1], hc = lh[lvl + 1];
-      StatePtrs cs = state_ptrs(fw.st[cur], fw.nb, cap);
+      const StatePtrs cs = state_ptrs(fw.st[cur], fw.nb, cap);
       cur = 1 - cur;
-      st = state_ptrs(fw.st[cur], fw.nb, cap);
-      k_upsample<<<grid2d(w, h, nb), blk, 0, s>>>(
-          cs.p[U1], cs.p[U2], wc, hc, st.p[U1], st.p[U2], w, h, cap, (double)wc / (double)w,
-          (double)hc / (double)h, (double)w / (double)wc, (double)h / (double)hc);
+      const StatePtrs st = state_ptrs(fw.st[cur], fw.nb, cap);
+      k_upsample<<<grid2d(w, h, nb), blk, 0, s>>>(cs.u, wc, hc, st.u, w, h, cap,
+                                                  (double)wc / (double)w, (double)hc / (double)h,
+                                                  (double)w / (double)wc, (double)h / (double)hc);
       count_launch();
     }
     const double *i0 = pyr0 + loff[lvl];
     const double *i1 = pyr1 + loff[lvl];
-    k_central_grad<<<grid2d(w, h, nb), blk, 0, s>>>(i1, w, h, pyr_stride, fw.ix, fw.iy, cap);
+    k_central_grad2<<<grid2d(w, h, nb), blk, 0, s>>>(i1, w, h, pyr_stride, fw.ix, cap);
     count_launch();
 
     const PDPlan plan = pd_plan(w, h);
     const bool resident = plan.halo == 0;
     const int halo = plan.halo;
-    // whole-level kernel for tiled levels whose tiles fit one cooperative
-    // launch (at least one stream per launch)
-    const int level_batch =
-        fw.level_ctas > 0 ? fw.level_ctas / level_pd_tiles(w, h) : 0;
-    const bool level = !resident && p.pd_kernel == FT_PD_AUTO && level_batch >= 1;
     PdSpan *span = lvl == 0 && !resident ? g_pd_span : nullptr;
     if (span) span->spans = span->launches = 0, span->pixel_iters = 0;
     for (int wp = 0; wp < p.warps; ++wp) {
-      st = state_ptrs(fw.st[cur], fw.nb, cap);
-      k_warp_setup<<<grid2d(w, h, nb), blk, 0, s>>>(i0, i1, pyr_stride, fw.ix, fw.iy, st.p[U1],
-                                                     st.p[U2], w, h, cap, fw.gx, fw.gy, fw.r0);
+      k_warp_setup<<<grid2d(w, h, nb), blk, 0, s>>>(i0, i1, pyr_stride, fw.ix,
+                                                     state_ptrs(fw.st[cur], fw.nb, cap).u, w, h,
+                                                     cap, tl, fw.g, fw.rt);
       count_launch();
       const int si = span && span->spans < PdSpan::kMaxSpans ? span->spans : -1;
       if (si >= 0)
         FT_CUDA_TRY(cudaEventRecordWithFlags(span->ev[2 * si], s, cudaEventRecordExternal));
-      if (level) {
-        // whole level on chip: one cooperative launch per batch of streams
-        StatePtrs in = state_ptrs(fw.st[cur], fw.nb, cap);
-        StatePtrs out = state_ptrs(fw.st[1 - cur], fw.nb, cap);
-        for (int b0 = 0; b0 < nb; b0 += level_batch) {
-          const int bn = std::min(level_batch, nb - b0);
-          const int64_t bo = (int64_t)b0 * cap;
-          LevelPDArgs la;
-          la.u1 = in.p[U1] + bo;
-          la.u2 = in.p[U2] + bo;
-          la.out1 = out.p[U1] + bo;
-          la.out2 = out.p[U2] + bo;
-          la.gx = fw.gx + bo;
-          la.gy = fw.gy + bo;
-          la.r0 = fw.r0 + bo;
-          la.w = w;
-          la.h = h;
-          la.cap = cap;
-          la.iters = p.iters;
-          la.tau = p.tau;
-          la.lam = p.lam;
-          la.sigma = sigma;
-          la.shrink = shrink;
-          la.edges = fw.edges;
-          la.flags = fw.flags;
-          la.err = fw.err;
-          FT_TRY(launch_level_pd(la, bn, pow2_params(p.tau), s));
-          if (si >= 0) ++span->launches;
-        }
-        cur = 1 - cur;
-      }
       // 2*iters half-steps D P D P ... split into launches that end after a
       // dual step (state u, p): the first of at most 2*halo-1 half-steps
       // (starts with D), then 2*halo (P..D), and the rest (odd, P..P) in the
       // last launch; a resident level runs them all in one launch.
-      const int total = level ? 0 : 2 * p.iters;
+      const int total = 2 * p.iters;
       int done = 0;
       while (done < total) {
         int n;
@@ -860,14 +936,8 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
         else if (done == 0) n = std::min(2 * halo - 1, total);
         else n = total - done <= 2 * halo ? total - done : 2 * halo;
         PDArgs a;
-        a.in = state_ptrs(fw.st[cur], fw.nb, cap);
-        a.out = state_ptrs(fw.st[1 - cur], fw.nb, cap);
-        a.gx = fw.gx;
-        a.gy = fw.gy;
-        a.r0 = fw.r0;
         a.w = w;
         a.h = h;
-        a.cap = cap;
         a.halo = halo;
         a.nb = nb;
         a.pow2 = pow2_params(p.tau);
@@ -877,7 +947,8 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
         a.lam = p.lam;
         a.sigma = sigma;
         a.shrink = shrink;
-        FT_TRY(pd_launch(plan.cfg, a, nb, s));
+        FT_TRY(pd_launch(plan.cfg, a, state_ptrs(fw.st[cur], fw.nb, cap),
+                         state_ptrs(fw.st[1 - cur], fw.nb, cap), fw.g, fw.rt, cap, nb, s));
         cur = 1 - cur;
         done += n;
         if (si >= 0) ++span->launches;
@@ -887,30 +958,24 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
         span->spans = si + 1;
         span->pixel_iters += (int64_t)w * h * nb * p.iters;
       }
-      StatePtrs in = state_ptrs(fw.st[cur], fw.nb, cap);
-      StatePtrs out = state_ptrs(fw.st[1 - cur], fw.nb, cap);
-      k_median<<<grid2d((w + 1) / 2, h, nb), blk, 0, s>>>(in.p[U1], in.p[U2], out.p[U1],
-                                                          out.p[U2], w, h, cap);
+      k_median<<<grid2d((w + 1) / 2, h, nb), blk, 0, s>>>(
+          state_ptrs(fw.st[cur], fw.nb, cap).u, state_ptrs(fw.st[1 - cur], fw.nb, cap).u, w, h,
+          cap);
       count_launch();
       cur = 1 - cur;
       if (energy_terms && lvl == 0 && nb == 1) {  // energy_trace (optflow.py:212-213)
         const int64_t n0 = (int64_t)w * h;
-        StatePtrs now = state_ptrs(fw.st[cur], fw.nb, cap);
+        const double *u = reinterpret_cast<const double *>(state_ptrs(fw.st[cur], fw.nb, cap).u);
         double *tb = energy_terms + (int64_t)wp * 3 * n0;
-        FT_TRY(launch_energy_terms(i0, i1, now.p[U1], now.p[U2], w, h, p.eps, tb, tb + n0,
-                                   tb + 2 * n0, s));
+        FT_TRY(launch_energy_terms(i0, i1, u, u + 1, 2, w, h, p.eps, tb, tb + n0, tb + 2 * n0, s));
       }
     }
     phase_mark(kLevelNames[lvl < 8 ? lvl : 7]);
   }
-  StatePtrs st = state_ptrs(fw.st[cur], fw.nb, cap);
   const int64_t n0 = (int64_t)lw[0] * lh[0];
-  for (int b = 0; b < nb; ++b) {
-    FT_CUDA_TRY(cudaMemcpyAsync(dx + b * out_stride, st.p[U1] + b * cap, n0 * 8,
-                                cudaMemcpyDeviceToDevice, s));
-    FT_CUDA_TRY(cudaMemcpyAsync(dy + b * out_stride, st.p[U2] + b * cap, n0 * 8,
-                                cudaMemcpyDeviceToDevice, s));
-  }
+  k_split<<<dim3(std::max<int64_t>(1, std::min<int64_t>((n0 + 255) / 256, 1184)), 1, nb), 256, 0,
+            s>>>(state_ptrs(fw.st[cur], fw.nb, cap).u, n0, cap, dx, dy, out_stride);
+  count_launch();
   FT_CUDA_TRY(cudaGetLastError());
   return FT_OK;
 }
@@ -919,10 +984,10 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
 
 namespace ft {
 int launch_energy_terms(const double *i0, const double *i1, const double *u1, const double *u2,
-                        int w, int h, double eps, double *data, double *s1, double *s2,
+                        int us, int w, int h, double eps, double *data, double *s1, double *s2,
                         cudaStream_t s) {
-  k_energy_terms<<<dim3((w + 31) / 32, (h + 7) / 8), dim3(32, 8), 0, s>>>(i0, i1, u1, u2, w, h, eps,
-                                                                       data, s1, s2);
+  k_energy_terms<<<dim3((w + 31) / 32, (h + 7) / 8), dim3(32, 8), 0, s>>>(i0, i1, u1, u2, us, w, h,
+                                                                       eps, data, s1, s2);
   count_launch();
   FT_CUDA_TRY(cudaGetLastError());
   return FT_OK;

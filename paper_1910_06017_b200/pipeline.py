@@ -37,13 +37,11 @@ class Tracker:
                  max_tracks: int = 512, max_dets: int = 512,
                  smoothing_weight: float = 12.0, blend: float = 0.05,
                  rof_iterations: int = 40, device: int | None = None,
-                 motion: str = "tvl1", klt_grid: int = 10, pd_kernel: str = "auto"):
+                 motion: str = "tvl1", klt_grid: int = 10):
         """motion="tvl1" is the reference path (structure-texture + TV-L1 +
         mean-box predict); motion="klt" swaps prediction for the KLT /
         MedianFlow backend (track.predict_klt) on the
-        processing-level frames -- matching and the lifecycle are shared.
-        pd_kernel ("auto" | "tiled") picks the primal-dual kernel of tiled
-        pyramid levels (bit-identical results; ft_flow_params.pd_kernel)."""
+        processing-level frames -- matching and the lifecycle are shared."""
         import torch
 
         self.width, self.height, self.n_streams = int(width), int(height), int(n_streams)
@@ -55,7 +53,7 @@ class Tracker:
         cfg = _lib.ft_tracker_config(
             self.width, self.height, self.n_streams, self.max_tracks, self.max_dets,
             int(rof_iterations), float(gate), float(min_score), float(detection_blend),
-            float(smoothing_weight), float(blend), _lib.flow_params_struct(flow_params, pd_kernel),
+            float(smoothing_weight), float(blend), _lib.flow_params_struct(flow_params),
             {"tvl1": _lib.MOTION_TVL1, "klt": _lib.MOTION_KLT}[motion], int(klt_grid))
         self.motion = motion
         h = C.c_void_p()

@@ -145,47 +145,6 @@ def test_flow_multitile_matches_oracle(pkg):
     assert np.array_equal(f.dx, odx) and np.array_equal(f.dy, ody)
 
 
-def _flow_with_kernel(a, b, prm, kernel):
-    """ft_compute_flow through the C ABI with an explicit primal-dual kernel
-    choice (ft_flow_params.pd_kernel)."""
-    import ctypes as C
-
-    import torch
-
-    from paper_1910_06017_b200 import _lib
-    da = torch.from_numpy(np.ascontiguousarray(a)).cuda()
-    db = torch.from_numpy(np.ascontiguousarray(b)).cuda()
-    dx, dy = torch.empty_like(da), torch.empty_like(da)
-    st = _lib.flow_params_struct(prm, kernel)
-    h, w = a.shape
-    _lib.check(_lib.load().ft_compute_flow(_lib.ctx(), _lib.ptr(da), _lib.ptr(db), w, h,
-                                           C.byref(st), _lib.ptr(dx), _lib.ptr(dy)))
-    return dx.cpu().numpy(), dy.cpu().numpy()
-
-
-@pytest.mark.parametrize("w,h,tau,iters", [
-    (720, 576, 0.25, 50),   # SD finest level: 12 x 24 tiles of the whole-level kernel
-    (203, 141, 0.25, 50),   # partial tiles on both axes, several levels tiled
-    (129, 65, 0.3, 13),     # non power-of-two time step (no fused products), odd iterations
-    (1300, 200, 0.25, 7),   # wide: 21 tile columns
-])
-def test_whole_level_kernel_matches_tiled(pkg, w, h, tau, iters):
-    """The whole-level primal-dual kernel (k_pd_level.cu: one cooperative
-    launch per warp, tile edges exchanged through L2) and the temporally
-    blocked tile kernel give the same bits, on ST-preprocessed frames."""
-    from paper_1910_06017_b200.synth import make_sequence
-    frames, _ = make_sequence(w, h, 6, 2, seed=w + h)
-    im, of = pkg.imaging, pkg.optflow
-    sa = np.asarray(im.structure_texture(im.Frame.from_gray8(frames[0])).data)
-    sb = np.asarray(im.structure_texture(im.Frame.from_gray8(frames[1])).data)
-    prm = of.FlowParams(time_step=tau, warps_per_level=2, iterations_per_warp=iters)
-    auto = _flow_with_kernel(sa, sb, prm, "auto")
-    tiled = _flow_with_kernel(sa, sb, prm, "tiled")
-    assert auto[0].tobytes() == tiled[0].tobytes()
-    assert auto[1].tobytes() == tiled[1].tobytes()
-    assert np.abs(auto[0]).max() > 0  # real motion
-
-
 def test_zero_motion_full_size(pkg):
     """Size-independent property at SD (720x576, default params): identical
     frames give an exactly zero field."""

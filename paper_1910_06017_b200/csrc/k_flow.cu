@@ -400,9 +400,8 @@ template <int TW, int BY, int PY, bool P2, bool IN, bool MID>
 __device__ __forceinline__ void pd_halfsteps_cq(const PDArgs &a, double *sm, int base, int tx,
                                                 int ty, const unsigned *fl, double *u1,
                                                 double *u2, const double *gx, const double *gy,
-                                                const double *r0, const double *thr,
-                                                const double *ig2, double tl, int *qidx,
-                                                int *ctr) {
+                                                const double2 *rt, const double *ig2, double tl,
+                                                int *qidx, int *ctr) {
   using G = PDGeom<TW, BY, PY>;
   constexpr int NX = G::NX, NP = G::NP, SP = G::SP, PL = G::PLANE, TH = G::TH;
   constexpr int NT = 32 * BY;
@@ -456,13 +455,13 @@ __device__ __forceinline__ void pd_halfsteps_cq(const PDArgs &a, double *sm, int
       // ---- append saturated pairs: one shared atomic per warp
       int off[2 * NP];
       int total = 0;
-      if (__any_sync(0xffffffffu, need != 0u)) {
 #pragma unroll
-        for (int k = 0; k < 2 * NP; ++k) {
-          const unsigned m = __ballot_sync(0xffffffffu, (need >> k) & 1u);
-          off[k] = total + __popc(m & lt_mask);
-          total += __popc(m);
-        }
+      for (int k = 0; k < 2 * NP; ++k) {
+        const unsigned m = __ballot_sync(0xffffffffu, (need >> k) & 1u);
+        off[k] = total + __popc(m & lt_mask);
+        total += __popc(m);
+      }
+      if (total) {  // warp-uniform
         int wbase = 0;
         if (tx == 0) wbase = atomicAdd(&ctr[nd & 1], total);
         wbase = __shfl_sync(0xffffffffu, wbase, 0);
@@ -502,9 +501,11 @@ __device__ __forceinline__ void pd_halfsteps_cq(const PDArgs &a, double *sm, int
         const double dy2 = U ? (LR ? -u22 : p22 - u22) : p22;
         const double v1 = madx<P2>(tau, dx1 + dy1, u1[q]);
         const double v2 = madx<P2>(tau, dx2 + dy2, u2[q]);
-        const double rho = r0[q] + gx[q] * v1 + gy[q] * v2;
-        const bool lo_ = rho < -thr[q];
-        const bool hi_ = rho > thr[q];
+        // (rho0, thresh) stay in the shared G/RT staging of the prologue
+        const double2 rq = rt[(ty + BY * (q / NX)) * TW + tx + 32 * (q % NX)];
+        const double rho = rq.x + gx[q] * v1 + gy[q] * v2;
+        const bool lo_ = rho < -rq.y;
+        const bool hi_ = rho > rq.y;
         double d = lo_ ? tl : (hi_ ? -tl : -rho * ig2[q]);
         d = (ig2[q] != 0.0 || lo_ || hi_) ? d : 0.0;  // ig2 != 0 <=> |grad|^2 > 1e-12
         const double n1 = v1 + d * gx[q];
@@ -588,10 +589,12 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const __grid_constant
     }
   }
   if (tid < 2) ctr[tid] = 0;
-  mbar_wait(bar, 0);
+  if (ty == 0) mbar_wait(bar, 0);  // one warp polls; the others sleep in the barrier
+  __syncthreads();
+  mbar_wait(bar, 0);  // completed phase: returns at once, orders the TMA data
 
   const double tl = a.tau * a.lam;
-  double u1[NP], u2[NP], gx[NP], gy[NP], r0[NP], thr[NP], ig2[NP];
+  double u1[NP], u2[NP], gx[NP], gy[NP], ig2[NP];
   unsigned fl[NP];
 #pragma unroll
   for (int k = 0; k < PY; ++k) {
@@ -602,13 +605,10 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const __grid_constant
       const int gc = ox + lc, gr = oy + lr;
       const double2 u = sB[base + k * BY * SP + 32 * cx];
       const double2 g = stage[lr * TW + lc];
-      const double2 rt = stage[TW * TH + lr * TW + lc];
       u1[q] = u.x;
       u2[q] = u.y;
       gx[q] = g.x;
       gy[q] = g.y;
-      r0[q] = rt.x;
-      thr[q] = rt.y;  // tau*lam*grad_sq (optflow.py:176), from the warp setup
       const double g2 = g.x * g.x + g.y * g.y;  // optflow.py:163-165
       ig2[q] = g2 > 1e-12 ? 1.0 / g2 : 0.0;
       fl[q] = (gc < W - 1 ? FL_R : 0u) | (gr < H - 1 ? FL_D : 0u) | (gc > 0 ? FL_L : 0u) |
@@ -621,8 +621,8 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const __grid_constant
   const bool interior = ox >= 1 && oy >= 1 && ox + TW <= W - 1 && oy + TH <= H - 1;
   {
 #define FT_PD_CALL(P2_, IN_)                                                                 \
-  pd_halfsteps_cq<TW, BY, PY, P2_, IN_, MID>(a, sm, base, tx, ty, fl, u1, u2, gx, gy, r0, thr, ig2, \
-                                        tl, qidx, ctr)
+  pd_halfsteps_cq<TW, BY, PY, P2_, IN_, MID>(a, sm, base, tx, ty, fl, u1, u2, gx, gy, \
+                                             stage + TW * TH, ig2, tl, qidx, ctr)
     if (a.pow2) {
       if (interior) FT_PD_CALL(true, true); else FT_PD_CALL(true, false);
     } else {

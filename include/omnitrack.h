@@ -39,6 +39,10 @@ extern "C" {
 #define FT_ENOMEM (-4) /* device / pinned allocation failed */
 #define FT_ECAP (-5)   /* tracker capacity (max_tracks / max_dets) exceeded */
 
+/* n_dets value of a stream that does not advance in a tracker step (no
+ * frame this step): its tracks, ids and previous frame stay as they are */
+#define FT_STREAM_SKIP (-2)
+
 /* optflow.py:36-66 FlowParams; pyramid_scales <= 0 means auto (optflow.py:96) */
 typedef struct ft_flow_params {
   double data_weight;   /* lambda, default 0.15 */
@@ -74,6 +78,11 @@ int ft_auto_scales(int width, int height, int *scales);  /* optflow.py:96-104 */
 /* ---- imaging (imaging.py) ----------------------------------------------- */
 /* Frame.from_gray8: u8/255 (imaging.py:52-56) */
 int ft_gray8_to_unit(ft_ctx *ctx, const uint8_t *d_src, int w, int h, double *d_dst);
+/* Frame / MotionField validation of device planes (imaging.py:33-44,
+ * optflow.py:85-86): *h_status = 0, or bit 0 when a value is non-finite, bit
+ * 1 when a finite value lies outside [lo, hi].  Synchronizes. */
+int ft_check_plane(ft_ctx *ctx, const double *d_plane, int64_t n, double lo, double hi,
+                   int32_t *h_status);
 /* build_pyramid (imaging.py:75-95): levels written back to back into
  * d_levels (level 0 copied), sizes floor-halved; FT_EINVAL below 2x2 */
 int ft_build_pyramid(ft_ctx *ctx, const double *d_frame, int w, int h, int num_levels,
@@ -184,7 +193,9 @@ int ft_tracker_create(ft_ctx *ctx, const ft_tracker_config *cfg, ft_tracker **ou
 int ft_tracker_destroy(ft_tracker *trk);
 /* One frame for every stream.  h_luma: n_streams x H x W u8 (host);
  * h_dets: n_streams x max_dets; h_n_dets[s] = -1 when stream s has no
- * detector result this frame (coast).  Outputs, per stream s, the active
+ * detector result this frame (coast), FT_STREAM_SKIP when stream s has no
+ * frame this step (it does not advance; its records are its unchanged
+ * active tracks).  Outputs, per stream s, the active
  * tracks followed by tracks that became lost this frame, into
  * h_out[s*(2*max_tracks) ...], count in h_n_out[s]. */
 int ft_tracker_step(ft_tracker *trk, const uint8_t *h_luma, int frame_index, const ft_det *h_dets,
@@ -205,6 +216,21 @@ int ft_tracker_slot_buffers(ft_tracker *trk, int slot, uint8_t **h_luma, ft_det 
                             int32_t **h_n_dets);
 int ft_tracker_submit(ft_tracker *trk, int slot, int frame_index, const uint8_t *h_luma,
                       const ft_det *h_dets, const int32_t *h_n_dets);
+/* Per-stream staging (SURVEY.md 8(b) ft_step(ctx, stream_id, luma, w, h,
+ * pitch, frame_index, dets, n_dets, ...)): copy stream `stream`'s W x H luma
+ * from rows `pitch` bytes apart, its detections (n_dets = -1 coast,
+ * FT_STREAM_SKIP no frame: luma may be NULL) and its frame index into the
+ * slot's pinned buffers.  ft_tracker_submit_staged then runs one step of
+ * every stream as staged (each with its own frame index). */
+int ft_tracker_stage(ft_tracker *trk, int slot, int stream, const uint8_t *h_luma, int pitch,
+                     int frame_index, const ft_det *h_dets, int n_dets);
+int ft_tracker_submit_staged(ft_tracker *trk, int slot);
+/* One step of a single stream (all others skip), synchronous: stream
+ * `stream`'s records (active tracks then the ones lost this step) into
+ * h_out (2 x max_tracks), count in *h_n_out. */
+int ft_tracker_step_stream(ft_tracker *trk, int stream, const uint8_t *h_luma, int pitch,
+                           int frame_index, const ft_det *h_dets, int n_dets, ft_track *h_out,
+                           int32_t *h_n_out);
 int ft_tracker_wait(ft_tracker *trk, int slot, ft_track *h_out, int32_t *h_n_out);
 /* Same step with inputs already resident on the device (d_luma as above,
  * d_dets/d_n_dets device arrays); no host copies, no synchronisation. */

@@ -16,6 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FT_LIB") or os.path.join(HERE, "libomnitrack.so")  # FT_LIB: A/B builds
 
 FT_OK, FT_EINVAL, FT_ERANGE, FT_ECUDA, FT_ENOMEM, FT_ECAP = 0, -1, -2, -3, -4, -5
+FT_STREAM_SKIP = -2  # n_dets of a stream that does not advance in a tracker step
 
 
 class OmniTrackError(RuntimeError):
@@ -79,6 +80,7 @@ SIGNATURES = {
     "ft_select_level": (_I, [_I, _I, C.POINTER(_I)]),
     "ft_auto_scales": (_I, [_I, _I, C.POINTER(_I)]),
     "ft_gray8_to_unit": (_I, [_P, _P, _I, _I, _P]),
+    "ft_check_plane": (_I, [_P, _P, C.c_int64, _D, _D, C.POINTER(C.c_int32)]),
     "ft_build_pyramid": (_I, [_P, _P, _I, _I, _I, _P]),
     "ft_structure_texture": (_I, [_P, _P, _I, _I, _D, _D, _I, _P]),
     "ft_rof_denoise": (_I, [_P, _P, _I, _I, _D, _I, _D, _P]),
@@ -99,6 +101,9 @@ SIGNATURES = {
     "ft_tracker_slot_buffers": (_I, [_P, _I, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P)]),
     "ft_tracker_submit": (_I, [_P, _I, _I, _P, _P, _P]),
     "ft_tracker_wait": (_I, [_P, _I, _P, _P]),
+    "ft_tracker_stage": (_I, [_P, _I, _I, _P, _I, _I, _P, _I]),
+    "ft_tracker_submit_staged": (_I, [_P, _I]),
+    "ft_tracker_step_stream": (_I, [_P, _I, _P, _I, _I, _P, _I, _P, C.POINTER(C.c_int32)]),
     "ft_tracker_read": (_I, [_P, _P, _P]),
     "ft_tracker_field": (_I, [_P, _I, C.POINTER(_P), C.POINTER(_P), C.POINTER(_I),
                               C.POINTER(_I)]),
@@ -168,6 +173,15 @@ def ctx(device: int | None = None):
     stream = torch.cuda.current_stream(dev).cuda_stream
     check(lib.ft_ctx_set_stream(h, C.c_void_p(stream)))
     return h
+
+
+def check_plane(t, lo: float, hi: float) -> int:
+    """Device-side Frame / MotionField validation of a CUDA float64 tensor:
+    0, or bit 0 = non-finite values, bit 1 = finite values outside [lo, hi]."""
+    st = C.c_int32()
+    check(load().ft_check_plane(ctx(t.device.index), ptr(t), t.numel(), float(lo), float(hi),
+                                C.byref(st)))
+    return st.value
 
 
 def ptr(a) -> C.c_void_p:

@@ -242,6 +242,20 @@ int ft_gray8_to_unit(ft_ctx *ctx, const uint8_t *src, int w, int h, double *dst)
   return launch_gray8_to_unit(src, w, h, 0, dst, 0, 1, ctx->stream);
 }
 
+int ft_check_plane(ft_ctx *ctx, const double *d, int64_t n, double lo, double hi,
+                   int32_t *h_status) {
+  if (!ctx || !h_status || (n > 0 && !d)) return fail(FT_EINVAL, "NULL argument");
+  *h_status = 0;
+  if (n <= 0) return FT_OK;
+  DeviceGuard g(ctx->device);
+  FT_TRY(ctx->ensure_scratch(64));
+  int *st = (int *)ctx->scratch;
+  FT_TRY(launch_check_plane(d, n, lo, hi, st, ctx->stream));
+  FT_CUDA_TRY(cudaMemcpyAsync(h_status, st, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  FT_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return FT_OK;
+}
+
 int ft_build_pyramid(ft_ctx *ctx, const double *frame, int w, int h, int levels, double *out) {
   if (!ctx || !frame || !out) return fail(FT_EINVAL, "NULL argument");
   FT_TRY(check_pyramid(w, h, levels));
@@ -595,7 +609,9 @@ struct ft_tracker {
   Geometry kgeo;
   double *d_kpts = nullptr, *d_kfwd = nullptr, *d_kfb = nullptr, *d_kbox = nullptr;
   ft_det *d_dets = nullptr;
-  int32_t *d_in = nullptr;  // [0] = frame index, [1..S] = n_dets
+  // [0] = frame index, [1..S] = n_dets (-1 coast, FT_STREAM_SKIP),
+  // [S+1..2S] = per-stream frame index
+  int32_t *d_in = nullptr;
   ft_track *d_out = nullptr;
   int32_t *d_nout = nullptr;
   TrackerDev T{};
@@ -670,7 +686,7 @@ struct ft_tracker {
       FT_CUDA_TRY(cudaMemcpyAsync(d_luma, h_luma, (size_t)S * W * H, cudaMemcpyHostToDevice, s));
       FT_CUDA_TRY(cudaMemcpyAsync(d_dets, h_dets, (size_t)S * cfg.max_dets * sizeof(ft_det),
                                   cudaMemcpyHostToDevice, s));
-      FT_CUDA_TRY(cudaMemcpyAsync(d_in, h_in, (size_t)(S + 1) * 4, cudaMemcpyHostToDevice, s));
+      FT_CUDA_TRY(cudaMemcpyAsync(d_in, h_in, (size_t)(2 * S + 1) * 4, cudaMemcpyHostToDevice, s));
       luma = d_luma;
       dets = d_dets;
       in = d_in;
@@ -694,6 +710,7 @@ struct ft_tracker {
     if (cfg.motion == FT_MOTION_KLT) {  // SURVEY 8 f4 backend: no ROF, no TV-L1
       KltArgs ka;
       FT_TRY(build_klt_pyramid(img, P, kgeo, pyr_cur, 3 * kgeo.total, S, s, ka.curr));
+      FT_TRY(launch_keep_prev(pyr_cur, pyr_prev, 3 * kgeo.total, in + 1, S, s));
       phase_mark("klt pyramid");
       const double *kbox = nullptr;
       if (has_prev) {
@@ -709,8 +726,8 @@ struct ft_tracker {
         kbox = d_kbox;
         phase_mark("klt track");
       }
-      FT_TRY(launch_tracker_track(T, nullptr, nullptr, P, PW, PH, L, dets, in + 1, in, has_prev,
-                                  d_out, d_nout, s, kbox));
+      FT_TRY(launch_tracker_track(T, nullptr, nullptr, P, PW, PH, L, dets, in + 1, in + 1 + S,
+                                  has_prev, d_out, d_nout, s, kbox));
       phase_mark("predict+match+update");
       if (host_io) {
         FT_CUDA_TRY(cudaMemcpyAsync(h_out, d_out,
@@ -726,6 +743,7 @@ struct ft_tracker {
     phase_mark("structure_texture");
     // (2) flow pyramid of the current ST frame (x255, optflow.py:242-243)
     FT_TRY(build_flow_pyramid(d_st, P, geo, d_fchain, pyr_cur, geo.total, S, s));
+    FT_TRY(launch_keep_prev(pyr_cur, pyr_prev, geo.total, in + 1, S, s));
     phase_mark("flow pyramid");
     // (3) feature calculation: TV-L1 between previous and current frame
     if (has_prev) {
@@ -735,8 +753,8 @@ struct ft_tracker {
                       geo.off.data(), scales, p, fw, d_dx, d_dy, P, S, s));
     }
     // (4) prediction, matching, update
-    FT_TRY(launch_tracker_track(T, d_dx, d_dy, P, PW, PH, L, dets, in + 1, in, has_prev, d_out,
-                                d_nout, s));
+    FT_TRY(launch_tracker_track(T, d_dx, d_dy, P, PW, PH, L, dets, in + 1, in + 1 + S, has_prev,
+                                d_out, d_nout, s));
     phase_mark("predict+match+update");
     if (host_io) {
       FT_CUDA_TRY(cudaMemcpyAsync(h_out, d_out, (size_t)S * 2 * cfg.max_tracks * sizeof(ft_track),
@@ -847,7 +865,7 @@ int ft_tracker_create(ft_ctx *ctx, const ft_tracker_config *cfg, ft_tracker **ou
   FT_TRY(t->alloc(&t->d_dx, (size_t)S * P));
   FT_TRY(t->alloc(&t->d_dy, (size_t)S * P));
   FT_TRY(t->alloc(&t->d_dets, (size_t)S * cfg->max_dets));
-  FT_TRY(t->alloc(&t->d_in, (size_t)S + 1));
+  FT_TRY(t->alloc(&t->d_in, (size_t)2 * S + 1));
   FT_TRY(t->alloc(&t->d_out, (size_t)S * 2 * cfg->max_tracks));
   FT_TRY(t->alloc(&t->d_nout, (size_t)2 * S));
   if (cfg->motion == FT_MOTION_KLT) {
@@ -911,7 +929,7 @@ int ft_tracker_create(ft_ctx *ctx, const ft_tracker_config *cfg, ft_tracker **ou
   for (auto &sl : t->slots) {
     FT_CUDA_TRY(cudaMallocHost(&sl.luma, (size_t)S * t->W * t->H));
     FT_CUDA_TRY(cudaMallocHost(&sl.dets, (size_t)S * D * sizeof(ft_det)));
-    FT_CUDA_TRY(cudaMallocHost(&sl.in, (size_t)(S + 1) * 4));
+    FT_CUDA_TRY(cudaMallocHost(&sl.in, (size_t)(2 * S + 1) * 4));
     FT_CUDA_TRY(cudaMallocHost(&sl.out, (size_t)S * 2 * C * sizeof(ft_track)));
     FT_CUDA_TRY(cudaMallocHost(&sl.nout, (size_t)2 * S * 4));
     FT_CUDA_TRY(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
@@ -979,23 +997,12 @@ int ft_tracker_slot_buffers(ft_tracker *t, int slot, uint8_t **luma, ft_det **de
   return FT_OK;
 }
 
-// Enqueue one step reading the inputs staged in `slot`; returns without
-// waiting.  Steps execute in submission order on the tracker's stream.
-int ft_tracker_submit(ft_tracker *t, int slot, int frame, const uint8_t *luma, const ft_det *dets,
-                      const int32_t *n_dets) {
-  if (!t || slot < 0 || slot > 1) return fail(FT_EINVAL, "bad tracker / slot");
+// Enqueue one step reading the inputs staged in `slot` (luma, detections,
+// n_dets and per-stream frame indices); returns without waiting.  Steps
+// execute in submission order on the tracker's stream.
+static int submit_slot(ft_tracker *t, int slot) {
   auto &sl = t->slots[slot];
-  if (sl.pending) return fail(FT_EINVAL, "slot still in flight: call ft_tracker_wait first");
-  const int S = t->S, D = t->cfg.max_dets;
-  const int32_t *nd = n_dets ? n_dets : sl.in + 1;
-  for (int s = 0; s < S; ++s)
-    if (nd[s] > D) return fail(FT_ECAP, "more detections than max_dets");
   DeviceGuard g(t->ctx->device);
-  // stage into the slot's pinned memory unless the caller wrote there directly
-  if (luma && luma != sl.luma) std::memcpy(sl.luma, luma, (size_t)S * t->W * t->H);
-  if (dets && dets != sl.dets) std::memcpy(sl.dets, dets, (size_t)S * D * sizeof(ft_det));
-  if (nd != sl.in + 1) std::memcpy(sl.in + 1, nd, (size_t)S * 4);
-  sl.in[0] = frame;
   t->use_slot(slot);
   FT_TRY(t->join_in());
   FT_TRY(t->run(t->frames_seen > 0, nullptr, nullptr, nullptr, true));
@@ -1005,6 +1012,59 @@ int ft_tracker_submit(ft_tracker *t, int slot, int frame, const uint8_t *luma, c
   sl.pending = true;
   t->frames_seen++;
   return FT_OK;
+}
+
+int ft_tracker_submit(ft_tracker *t, int slot, int frame, const uint8_t *luma, const ft_det *dets,
+                      const int32_t *n_dets) {
+  if (!t || slot < 0 || slot > 1) return fail(FT_EINVAL, "bad tracker / slot");
+  auto &sl = t->slots[slot];
+  if (sl.pending) return fail(FT_EINVAL, "slot still in flight: call ft_tracker_wait first");
+  const int S = t->S, D = t->cfg.max_dets;
+  const int32_t *nd = n_dets ? n_dets : sl.in + 1;
+  for (int s = 0; s < S; ++s) {
+    if (nd[s] > D) return fail(FT_ECAP, "more detections than max_dets");
+    if (nd[s] < FT_STREAM_SKIP) return fail(FT_EINVAL, "n_dets must be >= FT_STREAM_SKIP");
+  }
+  // stage into the slot's pinned memory unless the caller wrote there directly
+  if (luma && luma != sl.luma) std::memcpy(sl.luma, luma, (size_t)S * t->W * t->H);
+  if (dets && dets != sl.dets) std::memcpy(sl.dets, dets, (size_t)S * D * sizeof(ft_det));
+  if (nd != sl.in + 1) std::memcpy(sl.in + 1, nd, (size_t)S * 4);
+  sl.in[0] = frame;
+  for (int s = 0; s < S; ++s) sl.in[1 + S + s] = frame;
+  return submit_slot(t, slot);
+}
+
+int ft_tracker_stage(ft_tracker *t, int slot, int stream, const uint8_t *luma, int pitch,
+                     int frame, const ft_det *dets, int n_dets) {
+  if (!t || slot < 0 || slot > 1) return fail(FT_EINVAL, "bad tracker / slot");
+  auto &sl = t->slots[slot];
+  if (sl.pending) return fail(FT_EINVAL, "slot still in flight: call ft_tracker_wait first");
+  const int S = t->S, D = t->cfg.max_dets, W = t->W, H = t->H;
+  if (stream < 0 || stream >= S) return fail(FT_EINVAL, "stream out of range");
+  if (n_dets < FT_STREAM_SKIP) return fail(FT_EINVAL, "n_dets must be >= FT_STREAM_SKIP");
+  if (n_dets > D) return fail(FT_ECAP, "more detections than max_dets");
+  sl.in[1 + stream] = n_dets;
+  sl.in[1 + S + stream] = frame;
+  if (n_dets == FT_STREAM_SKIP) return FT_OK;  // no frame for this stream this step
+  if (!luma) return fail(FT_EINVAL, "NULL luma");
+  if (pitch < W) return fail(FT_EINVAL, "pitch must be >= width");
+  if (n_dets > 0 && !dets) return fail(FT_EINVAL, "NULL detections");
+  uint8_t *dst = sl.luma + (size_t)stream * W * H;
+  if (pitch == W) {
+    std::memcpy(dst, luma, (size_t)W * H);
+  } else {
+    for (int r = 0; r < H; ++r) std::memcpy(dst + (size_t)r * W, luma + (size_t)r * pitch, W);
+  }
+  if (n_dets > 0) std::memcpy(sl.dets + (size_t)stream * D, dets, (size_t)n_dets * sizeof(ft_det));
+  return FT_OK;
+}
+
+int ft_tracker_submit_staged(ft_tracker *t, int slot) {
+  if (!t || slot < 0 || slot > 1) return fail(FT_EINVAL, "bad tracker / slot");
+  if (t->slots[slot].pending) return fail(FT_EINVAL, "slot still in flight: call ft_tracker_wait first");
+  int32_t *in = t->slots[slot].in;
+  in[0] = in[1 + t->S];  // legacy global index: stream 0's
+  return submit_slot(t, slot);
 }
 
 // Wait for the step submitted in `slot` and return its track records.
@@ -1026,17 +1086,40 @@ int ft_tracker_step(ft_tracker *t, const uint8_t *luma, int frame, const ft_det 
   return ft_tracker_wait(t, 0, out, n_out);
 }
 
+int ft_tracker_step_stream(ft_tracker *t, int stream, const uint8_t *luma, int pitch, int frame,
+                           const ft_det *dets, int n_dets, ft_track *out, int32_t *n_out) {
+  if (!t || !out || !n_out) return fail(FT_EINVAL, "NULL argument");
+  if (stream < 0 || stream >= t->S) return fail(FT_EINVAL, "stream out of range");
+  if (n_dets == FT_STREAM_SKIP) return fail(FT_EINVAL, "a stepped stream cannot be skipped");
+  auto &sl = t->slots[0];
+  if (sl.pending) return fail(FT_EINVAL, "slot still in flight: call ft_tracker_wait first");
+  for (int s = 0; s < t->S; ++s) sl.in[1 + s] = FT_STREAM_SKIP;
+  FT_TRY(ft_tracker_stage(t, 0, stream, luma, pitch, frame, dets, n_dets));
+  FT_TRY(ft_tracker_submit_staged(t, 0));
+  DeviceGuard g(t->ctx->device);
+  FT_CUDA_TRY(cudaEventSynchronize(sl.done));
+  sl.pending = false;
+  t->use_slot(0);
+  const int C = t->cfg.max_tracks;
+  const int n = t->h_nout[stream];
+  std::memcpy(out, t->h_out + (size_t)stream * 2 * C, (size_t)n * sizeof(ft_track));
+  *n_out = n;
+  if (t->h_nout[t->S + stream]) return fail(FT_ECAP, "stream " + std::to_string(stream) +
+                                                          " exceeded max_tracks");
+  return FT_OK;
+}
+
 int ft_tracker_step_device(ft_tracker *t, const uint8_t *d_luma, int frame, const ft_det *d_dets,
                            const int32_t *d_n_dets) {
   if (!t || !d_luma || !d_dets || !d_n_dets) return fail(FT_EINVAL, "NULL argument");
   DeviceGuard g(t->ctx->device);
   // gather the caller's device inputs into the tracker's fixed input buffers
   // (D2D, ~HBM speed) so one captured graph serves every step; the frame
-  // index travels in d_in[0] (pageable source: staged before return).
+  // index is written into d_in by a fill kernel (passed by value).
   cudaStream_t s = t->stream;
   FT_TRY(t->join_in());
-  const int32_t fr = frame;
-  FT_CUDA_TRY(cudaMemcpyAsync(t->d_in, &fr, 4, cudaMemcpyHostToDevice, s));
+  FT_TRY(launch_fill_i32(t->d_in, 1, frame, s));
+  FT_TRY(launch_fill_i32(t->d_in + 1 + t->S, t->S, frame, s));
   FT_CUDA_TRY(cudaMemcpyAsync(t->d_in + 1, d_n_dets, (size_t)t->S * 4, cudaMemcpyDeviceToDevice, s));
   FT_CUDA_TRY(cudaMemcpyAsync(t->d_luma, d_luma, (size_t)t->S * t->W * t->H,
                               cudaMemcpyDeviceToDevice, s));

@@ -138,6 +138,8 @@ inline void phase_mark(const char *what) {
 // ---------------------------------------------------------------- imaging
 // All batched launchers operate on `nb` independent images laid out with a
 // fixed element stride between consecutive images.
+int launch_check_plane(const double *d, int64_t n, double lo, double hi, int *status,
+                       cudaStream_t s);
 int launch_gray8_to_unit(const uint8_t *src, int w, int h, int64_t src_stride, double *dst,
                          int64_t dst_stride, int nb, cudaStream_t s);
 // one pyramid step: dst = decimate2(smooth_gaussian5(src)); optional scaled copy

@@ -37,9 +37,14 @@ __device__ __forceinline__ void copy_track(TrackerDev &T, int64_t d, int64_t s) 
 
 int launch_tracker_track(TrackerDev &T, const double *dx, const double *dy, int64_t fstride,
                          int fw_l, int fh_l, int level, const ft_det *d_dets,
-                         const int32_t *d_ndets, const int32_t *d_frame, bool has_prev,
+                         const int32_t *d_ndets, const int32_t *d_frames, bool has_prev,
                          ft_track *d_out, int32_t *d_nout, cudaStream_t s,
                          const double *kbox = nullptr);
 int tracker_kernel_setup(const TrackerDev &T);
+// dst[0..n) = v
+int launch_fill_i32(int32_t *dst, int n, int32_t v, cudaStream_t s);
+// per stream s with n_dets[s] == FT_STREAM_SKIP: cur[s] = prev[s]
+int launch_keep_prev(double *cur, const double *prev, int64_t per_stream, const int32_t *n_dets,
+                     int n_streams, cudaStream_t s);
 
 }  // namespace ft

@@ -292,6 +292,29 @@ int grid1d(int64_t n, int bs) {
 
 }  // namespace
 
+// Frame / MotionField validation: OR of (non-finite -> 1, outside [lo, hi] -> 2)
+__global__ void k_check_plane(const double *__restrict__ d, int64_t n, double lo, double hi,
+                              int *status) {
+  int f = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = d[i];
+    if (!isfinite(v)) f |= 1;
+    else if (v < lo || v > hi) f |= 2;
+  }
+  f = __reduce_or_sync(0xffffffffu, f);
+  if ((threadIdx.x & 31) == 0 && f) atomicOr(status, f);
+}
+
+int launch_check_plane(const double *d, int64_t n, double lo, double hi, int *status,
+                       cudaStream_t s) {
+  FT_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int), s));
+  k_check_plane<<<grid1d(n, 256), 256, 0, s>>>(d, n, lo, hi, status);
+  count_launch();
+  FT_CUDA_TRY(cudaGetLastError());
+  return FT_OK;
+}
+
 int launch_gray8_to_unit(const uint8_t *src, int w, int h, int64_t ss, double *dst, int64_t ds,
                          int nb, cudaStream_t s) {
   // 8 pixels per thread on the vector path

@@ -2,6 +2,7 @@
 // cost (assoc.py:30-41, :119-126), exact Hungarian (assoc.py:44-106) and the
 // lifecycle update (track.py:90-139), plus their batched multi-stream forms
 // used by the tracker step.
+#include <algorithm>
 #include <cfloat>
 #include <math_constants.h>
 
@@ -496,11 +497,12 @@ int launch_hungarian(const double *cost, int m, int n, int has_forbidden, double
 // (grid.x = stream, grid.y covers 2*cap items) -> window mean in T.pmean
 __global__ void __launch_bounds__(32 * kPredWarps)
     k_trk_predict(TrackerDev T, const double *dx, const double *dy, int64_t field_stride, int fw_l,
-                  int fh_l, int level) {
+                  int fh_l, int level, const int32_t *n_dets) {
   extern __shared__ __align__(16) char smem[];
   const int warp = threadIdx.x >> 5;
   LeafScratch &L = reinterpret_cast<LeafScratch *>(smem)[warp];
   const int s = blockIdx.x;
+  if (n_dets[s] == FT_STREAM_SKIP) return;  // the stream does not advance this step
   const int item = blockIdx.y * kPredWarps + warp;
   const int i = item >> 1, comp = item & 1;
   if (i >= T.n_active[s]) return;
@@ -517,8 +519,9 @@ __global__ void __launch_bounds__(32 * kPredWarps)
 // predict, phase 2: apply valid predictions (track.py:82-86), then build the
 // candidate list (actives with a prediction, table order) -- SURVEY A16 (4)
 // kbox != null: the KLT backend already produced the predicted boxes
-__global__ void k_trk_apply(TrackerDev T, int level, const double *kbox) {
+__global__ void k_trk_apply(TrackerDev T, int level, const double *kbox, const int32_t *n_dets) {
   const int s = blockIdx.x;
+  if (n_dets[s] == FT_STREAM_SKIP) return;
   const int na = T.n_active[s];
   const int64_t tb = (int64_t)s * T.cap;
   for (int i = threadIdx.x; i < na; i += blockDim.x) {
@@ -598,14 +601,14 @@ __global__ void k_trk_hungarian(TrackerDev T, const int32_t *n_dets) {
 // emitted to the per-stream lost list and compacted out (they never re-enter
 // matching and only their ids matter, via next_id).
 __global__ void k_trk_update(TrackerDev T, const ft_det *dets, const int32_t *n_dets,
-                             const int32_t *d_frame) {
+                             const int32_t *frames) {
   const int s = blockIdx.x;
   if (threadIdx.x != 0) return;
-  const int frame = *d_frame;
+  const int frame = frames[s];
   const int nd_raw = n_dets[s];
   const int64_t tb = (int64_t)s * T.cap;
   T.n_lost[s] = 0;
-  if (nd_raw < 0) return;
+  if (nd_raw < 0) return;  // coast (-1) or not advancing (FT_STREAM_SKIP)
   const ft_det *D = dets + (int64_t)s * T.max_dets;
   const int32_t *kept = T.kept + (int64_t)s * T.max_dets;
   const int nk = T.n_kept[s], nc = T.n_cand[s], na = T.n_active[s];
@@ -711,19 +714,51 @@ __global__ void k_trk_pack(TrackerDev T, ft_track *out, int32_t *n_out) {
   if (threadIdx.x == 0) n_out[s] = na + nl;
 }
 
+// Streams that do not advance this step keep their previous pyramid: the
+// step built into the other ping-pong buffer, so copy theirs across.
+__global__ void k_keep_prev(double *cur, const double *prev, int64_t per_stream,
+                            const int32_t *n_dets) {
+  const int s = blockIdx.y;
+  if (n_dets[s] != FT_STREAM_SKIP) return;
+  const int64_t o = (int64_t)s * per_stream;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < per_stream;
+       i += (int64_t)gridDim.x * blockDim.x)
+    cur[o + i] = prev[o + i];
+}
+
+__global__ void k_fill_i32(int32_t *dst, int n, int32_t v) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = v;
+}
+
+int launch_fill_i32(int32_t *dst, int n, int32_t v, cudaStream_t s) {
+  k_fill_i32<<<(n + 255) / 256, 256, 0, s>>>(dst, n, v);
+  count_launch();
+  FT_CUDA_TRY(cudaGetLastError());
+  return FT_OK;
+}
+
+int launch_keep_prev(double *cur, const double *prev, int64_t per_stream, const int32_t *n_dets,
+                     int n_streams, cudaStream_t s) {
+  const int bx = (int)std::min<int64_t>((per_stream + 255) / 256, 64);
+  k_keep_prev<<<dim3(bx, n_streams), 256, 0, s>>>(cur, prev, per_stream, n_dets);
+  count_launch();
+  FT_CUDA_TRY(cudaGetLastError());
+  return FT_OK;
+}
+
 int launch_tracker_track(TrackerDev &T, const double *dx, const double *dy, int64_t fstride,
                          int fw_l, int fh_l, int level, const ft_det *d_dets,
-                         const int32_t *d_ndets, const int32_t *d_frame, bool has_prev,
+                         const int32_t *d_ndets, const int32_t *d_frames, bool has_prev,
                          ft_track *d_out, int32_t *d_nout, cudaStream_t s, const double *kbox) {
   const int S = T.n_streams;
   if (has_prev && kbox) {  // KLT backend: boxes + valid already predicted
-    k_trk_apply<<<S, 128, 0, s>>>(T, level, kbox);
+    k_trk_apply<<<S, 128, 0, s>>>(T, level, kbox, d_ndets);
     count_launch();
   } else if (has_prev) {
     const dim3 pg(S, (2 * T.cap + kPredWarps - 1) / kPredWarps);
     k_trk_predict<<<pg, 32 * kPredWarps, kPredWarps * sizeof(LeafScratch), s>>>(
-        T, dx, dy, fstride, fw_l, fh_l, level);
-    k_trk_apply<<<S, 128, 0, s>>>(T, level, nullptr);
+        T, dx, dy, fstride, fw_l, fh_l, level, d_ndets);
+    k_trk_apply<<<S, 128, 0, s>>>(T, level, nullptr, d_ndets);
     count_launch(2);
   } else {
     // first frame: nothing to predict, every kept detection spawns
@@ -735,7 +770,7 @@ int launch_tracker_track(TrackerDev &T, const double *dx, const double *dy, int6
   const size_t sm = hungarian_smem(T.cap, T.max_dets);
   k_trk_hungarian<<<S, 32, sm, s>>>(T, d_ndets);
   count_launch();
-  k_trk_update<<<S, 32, 0, s>>>(T, d_dets, d_ndets, d_frame);
+  k_trk_update<<<S, 32, 0, s>>>(T, d_dets, d_ndets, d_frames);
   count_launch();
   k_trk_pack<<<S, 128, 0, s>>>(T, d_out, d_nout);
   count_launch();

@@ -43,7 +43,17 @@ class Frame:
             if tuple(data.shape) != (self.height, self.width):
                 raise ValueError(f"frame data shape {tuple(data.shape)} does not match "
                                  f"{self.height}x{self.width}")
-            object.__setattr__(self, "_dev", data.to(torch.float64).contiguous())
+            dev = data.to(torch.float64).contiguous()
+            if not dev.is_cuda:
+                dev = dev.cuda()
+            # the reference validates every Frame (imaging.py:33-44): same
+            # checks on the device (one reduction, one 4-byte read back)
+            bad = _lib.check_plane(dev, 0.0, 1.0)
+            if bad & 1:
+                raise ValueError("frame contains non-finite values")
+            if bad & 2:
+                raise ValueError("frame values must lie in [0, 1]")
+            object.__setattr__(self, "_dev", dev)
             object.__setattr__(self, "_host", None)
             return
         arr = np.ascontiguousarray(data, dtype=np.float64)
@@ -89,7 +99,7 @@ class Frame:
         torch = _torch()
         u8 = np.ascontiguousarray(data, dtype=np.uint8)
         h, w = u8.shape
-        src = torch.from_numpy(u8).cuda()
+        src = torch.from_numpy(u8 if u8.flags.writeable else u8.copy()).cuda()
         dst = torch.empty((h, w), dtype=torch.float64, device=src.device)
         _lib.check(_lib.load().ft_gray8_to_unit(_lib.ctx(), _lib.ptr(src), w, h, _lib.ptr(dst)))
         return cls(width=w, height=h, index=index, data=dst)

@@ -60,6 +60,10 @@ class MotionField:
         if on_dev:
             if tuple(dx.shape) != shape or tuple(dy.shape) != shape:
                 raise ValueError(f"field components must be {shape}")
+            # optflow.py:85-86 rejects non-finite fields at construction
+            # (inside compute_flow): checked on the device
+            if _lib.check_plane(dx, -np.inf, np.inf) | _lib.check_plane(dy, -np.inf, np.inf):
+                raise ValueError("field contains non-finite values")
             object.__setattr__(self, "_ddx", dx)
             object.__setattr__(self, "_ddy", dy)
             object.__setattr__(self, "_dx", None)
@@ -87,8 +91,6 @@ class MotionField:
         if self._dx is None:
             dx = self._ddx.cpu().numpy()
             dy = self._ddy.cpu().numpy()
-            if not (np.all(np.isfinite(dx)) and np.all(np.isfinite(dy))):
-                raise ValueError("field contains non-finite values")
             dx.setflags(write=False)
             dy.setflags(write=False)
             object.__setattr__(self, "_dx", dx)

@@ -107,62 +107,127 @@ class Tracker:
             self._label_names.append(label)
         return ref
 
-    def _stage(self, frames, detections, slot: int = 0):
+    def _det_records(self, dets) -> np.ndarray:
+        if isinstance(dets, np.ndarray) and dets.dtype == _lib.DET_DTYPE:
+            rec = dets
+        else:
+            rec = np.zeros(len(dets), dtype=_lib.DET_DTYPE)
+            for j, d in enumerate(dets):
+                rec[j] = (d.class_id, self._label_ref(d.label), d.score, *d.box)
+        if len(rec) > self.max_dets:
+            raise ValueError(f"{len(rec)} detections exceed max_dets={self.max_dets}")
+        return rec
+
+    def _stage(self, frames, detections, slot: int = 0, frame_index=None) -> bool:
+        """Stage one step's inputs into pinned slot `slot`.  Returns True when
+        the per-stream path was used (submit with ft_tracker_submit_staged).
+
+        frames: an (S, H, W) u8 array (every stream advances), or a list of S
+        entries -- a 2-D u8 array per stream (rows may be pitched, e.g. a crop
+        of a larger buffer) or None for a stream with no frame this step (it
+        does not advance: FT_STREAM_SKIP).  frame_index: an int, or one per
+        stream for the per-stream path."""
         S = self.n_streams
         luma_in, dets_in, ndets_in = self._slots[slot]
+        if detections is None:
+            detections = [None] * S
+        if len(detections) != S:
+            raise ValueError(f"need one detection list (or None) per stream ({S})")
+        if isinstance(frames, (list, tuple)):
+            if len(frames) != S:
+                raise ValueError(f"need one frame (or None) per stream ({S})")
+            idx = ([int(frame_index)] * S if np.ndim(frame_index) == 0
+                   else [int(v) for v in frame_index])
+            if len(idx) != S:
+                raise ValueError(f"need one frame index per stream ({S})")
+            for s, (f, dets) in enumerate(zip(frames, detections)):
+                if f is None:
+                    _lib.check(self._lib.ft_tracker_stage(self._h, slot, s, None, 0, idx[s], None,
+                                                          _lib.FT_STREAM_SKIP))
+                    continue
+                f = np.asarray(f)
+                if f.dtype != np.uint8 or f.shape != (self.height, self.width) or \
+                        f.strides[1] != 1:
+                    f = np.ascontiguousarray(f, dtype=np.uint8)
+                    if f.shape != (self.height, self.width):
+                        raise ValueError(f"stream {s}: frame must be {(self.height, self.width)}, "
+                                         f"got {f.shape}")
+                if dets is None:
+                    rec, n = None, -1
+                else:
+                    rec = self._det_records(dets)
+                    n = len(rec)
+                _lib.check(self._lib.ft_tracker_stage(
+                    self._h, slot, s, _lib.ptr(f), int(f.strides[0]), idx[s],
+                    None if rec is None or n == 0 else _lib.ptr(rec), n))
+            return True
         frames = np.asarray(frames, dtype=np.uint8)
         if frames.ndim == 2:
             frames = frames[None]
         if frames.shape != (S, self.height, self.width):
             raise ValueError(f"frames must be {(S, self.height, self.width)}, got {frames.shape}")
         luma_in[...] = frames
-        if detections is None:
-            detections = [None] * S
-        if len(detections) != S:
-            raise ValueError(f"need one detection list (or None) per stream ({S})")
         for s, dets in enumerate(detections):
             if dets is None:
                 ndets_in[s] = -1
                 continue
-            if isinstance(dets, np.ndarray) and dets.dtype == _lib.DET_DTYPE:
-                n = len(dets)
-                if n > self.max_dets:
-                    raise ValueError(f"{n} detections exceed max_dets={self.max_dets}")
-                dets_in[s, :n] = dets
-                ndets_in[s] = n
-                continue
-            n = len(dets)
-            if n > self.max_dets:
-                raise ValueError(f"{n} detections exceed max_dets={self.max_dets}")
-            rec = dets_in[s]
-            for j, d in enumerate(dets):
-                rec[j] = (d.class_id, self._label_ref(d.label), d.score, *d.box)
-            ndets_in[s] = n
+            rec = self._det_records(dets)
+            dets_in[s, :len(rec)] = rec
+            ndets_in[s] = len(rec)
+        return False
 
-    def step_records(self, frames, frame_index: int, detections=None):
-        """One frame for every stream; returns a list (per stream) of
-        TRACK_DTYPE record arrays: the active tracks in scene order followed
-        by the tracks that turned Lost this frame."""
+    def step_records(self, frames, frame_index, detections=None):
+        """One step; returns a list (per stream) of TRACK_DTYPE record arrays:
+        the active tracks in scene order followed by the tracks that turned
+        Lost this frame (a stream without a frame this step returns its
+        unchanged active tracks).  See _stage for the accepted inputs."""
         if self._pending:  # slot 0's pinned inputs may still feed an in-flight step
             raise RuntimeError(f"{len(self._pending)} submitted step(s) in flight: call wait() "
                                "before a synchronous step")
-        self._stage(frames, detections)
-        _lib.check(self._lib.ft_tracker_step(
-            self._h, _lib.ptr(self.luma_in), int(frame_index), _lib.ptr(self.dets_in),
-            _lib.ptr(self.ndets_in), _lib.ptr(self._out), _lib.ptr(self._nout)))
+        if self._stage(frames, detections, 0, frame_index):
+            _lib.check(self._lib.ft_tracker_submit_staged(self._h, 0))
+            _lib.check(self._lib.ft_tracker_wait(self._h, 0, _lib.ptr(self._out),
+                                                 _lib.ptr(self._nout)))
+        else:
+            _lib.check(self._lib.ft_tracker_step(
+                self._h, _lib.ptr(self.luma_in), int(frame_index), _lib.ptr(self.dets_in),
+                _lib.ptr(self.ndets_in), _lib.ptr(self._out), _lib.ptr(self._nout)))
         self._frame = frame_index
         return [self._out[s, :self._nout[s]] for s in range(self.n_streams)]
 
+    def step_stream(self, stream: int, frame, frame_index: int, detections=None):
+        """One step of a single stream (SURVEY 8(b) ft_step): the other
+        streams do not advance.  `frame` may be a pitched 2-D u8 array.
+        Returns that stream's full scene list (like step())."""
+        if self._pending:
+            raise RuntimeError("submitted steps in flight: call wait() first")
+        f = np.asarray(frame)
+        if f.dtype != np.uint8 or f.shape != (self.height, self.width) or f.strides[1] != 1:
+            f = np.ascontiguousarray(f, dtype=np.uint8)
+        rec = None if detections is None else self._det_records(detections)
+        n = -1 if rec is None else len(rec)
+        out = np.zeros(2 * self.max_tracks, dtype=_lib.TRACK_DTYPE)
+        cnt = C.c_int32()
+        _lib.check(self._lib.ft_tracker_step_stream(
+            self._h, int(stream), _lib.ptr(f), int(f.strides[0]), int(frame_index),
+            None if not n or rec is None else _lib.ptr(rec), n, _lib.ptr(out), C.byref(cnt)))
+        recs = [None] * self.n_streams
+        recs[stream] = out[:cnt.value]
+        return self.scenes(recs, streams=(stream,))[stream]
+
     # ------------------------------------------------------------------ async
-    def submit(self, frames, frame_index: int, detections=None) -> None:
-        """Stage one frame per stream into the next pinned slot and enqueue
-        the step without waiting (at most two in flight).  Results come
-        back, in order, from `wait()`; they equal step_records' output."""
+    def submit(self, frames, frame_index, detections=None) -> None:
+        """Stage one step (see _stage) into the next pinned slot and enqueue
+        it without waiting (at most two in flight).  Results come back, in
+        order, from `wait()`; they equal step_records' output."""
         if len(self._pending) == 2:
             raise RuntimeError("two steps in flight: call wait() first")
         slot = self._next_slot
-        self._stage(frames, detections, slot)
-        _lib.check(self._lib.ft_tracker_submit(self._h, slot, int(frame_index), None, None, None))
+        if self._stage(frames, detections, slot, frame_index):
+            _lib.check(self._lib.ft_tracker_submit_staged(self._h, slot))
+        else:
+            _lib.check(self._lib.ft_tracker_submit(self._h, slot, int(frame_index), None, None,
+                                                   None))
         self._pending.append(slot)
         self._next_slot ^= 1
 
@@ -179,10 +244,13 @@ class Tracker:
         the reference's scene after `update`."""
         return self.scenes(self.step_records(frames, frame_index, detections))
 
-    def scenes(self, recs):
+    def scenes(self, recs, streams=None):
         """Full scene lists from one step's records (keeps the tombstones)."""
         scenes = []
         for s, r in enumerate(recs):
+            if streams is not None and s not in streams:
+                scenes.append(None)
+                continue
             active, newly_lost = [], []
             for row in r:
                 obj = self._obj(row)

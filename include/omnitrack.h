@@ -184,6 +184,14 @@ typedef struct ft_tracker_config {
   ft_flow_params flow;
   int32_t motion;   /* FT_MOTION_TVL1 (reference path) or FT_MOTION_KLT */
   int32_t klt_grid; /* KLT points per box side (1..11), default 10 */
+  /* 1: device prefetch (TV-L1 only): the graph
+   * of the step submitted with frame t preprocesses frame t while the flow,
+   * predict, match and update of frame t-1 run concurrently on a second
+   * stream; ft_tracker_wait returns frame t-1's records (none after the
+   * first frame) and ft_tracker_flush tracks the last frame.  Results are
+   * identical to the sequential mode. */
+  int32_t prefetch;
+  int32_t _pad;
 } ft_tracker_config;
 
 #define FT_MOTION_TVL1 0
@@ -225,6 +233,9 @@ int ft_tracker_submit(ft_tracker *trk, int slot, int frame_index, const uint8_t 
 int ft_tracker_stage(ft_tracker *trk, int slot, int stream, const uint8_t *h_luma, int pitch,
                      int frame_index, const ft_det *h_dets, int n_dets);
 int ft_tracker_submit_staged(ft_tracker *trk, int slot);
+/* Prefetch trackers: a step with no new frame that tracks the pending last
+ * frame (its records come back from ft_tracker_wait on `slot`). */
+int ft_tracker_flush(ft_tracker *trk, int slot);
 /* One step of a single stream (all others skip), synchronous: stream
  * `stream`'s records (active tracks then the ones lost this step) into
  * h_out (2 x max_tracks), count in *h_n_out. */

@@ -48,7 +48,8 @@ class ft_tracker_config(C.Structure):
                 ("rof_iterations", C.c_int32), ("gate", C.c_double),
                 ("min_score", C.c_double), ("detection_blend", C.c_double),
                 ("rof_weight", C.c_double), ("rof_blend", C.c_double),
-                ("flow", ft_flow_params), ("motion", C.c_int32), ("klt_grid", C.c_int32)]
+                ("flow", ft_flow_params), ("motion", C.c_int32), ("klt_grid", C.c_int32),
+                ("prefetch", C.c_int32), ("_pad", C.c_int32)]
 
 
 MOTION_TVL1, MOTION_KLT = 0, 1
@@ -103,6 +104,7 @@ SIGNATURES = {
     "ft_tracker_wait": (_I, [_P, _I, _P, _P]),
     "ft_tracker_stage": (_I, [_P, _I, _I, _P, _I, _I, _P, _I]),
     "ft_tracker_submit_staged": (_I, [_P, _I]),
+    "ft_tracker_flush": (_I, [_P, _I]),
     "ft_tracker_step_stream": (_I, [_P, _I, _P, _I, _I, _P, _I, _P, C.POINTER(C.c_int32)]),
     "ft_tracker_read": (_I, [_P, _P, _P]),
     "ft_tracker_field": (_I, [_P, _I, C.POINTER(_P), C.POINTER(_P), C.POINTER(_I),

@@ -616,6 +616,22 @@ struct ft_tracker {
   int32_t *d_nout = nullptr;
   TrackerDev T{};
   FlowWork fw;
+  // ---- device prefetch (cfg.prefetch, TV-L1 only, SPEC.md
+  // :418): the graph of step k forks -- preprocessing of frame k on `stream`,
+  // flow + predict/match/update of frame k-1 on `stream2` -- and joins; the
+  // records of frame k-1 come back with step k (one-frame lag), a flush step
+  // tracks the last frame.  Three rotating flow pyramids (frame k being
+  // built, k-1 and k-2 being read) and per-parity device inputs.
+  int prefetch = 0;
+  cudaStream_t stream2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  double *d_pyr3[3] = {};
+  ft_det *d_dets2[2] = {};
+  int32_t *d_in2[2] = {};
+  int pf_prev = 0, pf_pend = 1;  // pyramid buffers of frames k-2 and k-1
+  bool pf_pending = false;       // a preprocessed frame awaits tracking
+  int64_t pf_tracked = 0;        // frames tracked since reset
+  int pf_par = 0;                // parity of the next step's device inputs
   // pinned staging, double-buffered: slot k holds the inputs / outputs of
   // every submission with frame parity k so the host can stage frame t+1
   // while the device runs frame t (ft_tracker_submit / ft_tracker_wait).
@@ -628,6 +644,7 @@ struct ft_tracker {
     int32_t *nout = nullptr;
     cudaEvent_t done = nullptr;
     bool pending = false;
+    bool records = true;          // the submission produces track records
     const void *graph = nullptr;  // Graph of the slot's last submission
   } slots[2];
   uint8_t *h_luma = nullptr;
@@ -645,7 +662,9 @@ struct ft_tracker {
   // graphs keyed by (has_prev, input pointers)
   int pyr_par = 0;  // which pyramid buffer is current (flips every step)
   struct GraphKey {
-    int has_prev;  // bit 0: has a previous frame; bit 1: pyramid parity
+    // bit 0: has a previous frame; bit 1: pyramid parity; prefetch graphs:
+    // bits 2.. new frame / track / buffer indices / input parity
+    int has_prev;
     const void *luma, *dets, *in;
     bool operator<(const GraphKey &o) const {
       if (has_prev != o.has_prev) return has_prev < o.has_prev;
@@ -765,13 +784,79 @@ struct ft_tracker {
     return FT_OK;
   }
 
-  int run(bool has_prev, const uint8_t *luma, const ft_det *dets, const int32_t *in,
-          bool host_io) {
+  // preprocessing of the current step's frame (imaging.py:75-144 + flow
+  // pyramid) into `pyr` for every stream; streams that skip keep `pyr_keep`
+  int enqueue_preprocess(cudaStream_t s, const uint8_t *luma, const int32_t *in, double *pyr,
+                         const double *pyr_keep) {
+    const double *img;
+    if (L == 0) {
+      FT_TRY(launch_gray8_to_unit(luma, W, H, (int64_t)W * H, d_chain[0], P, S, s));
+      img = d_chain[0];
+    } else {
+      FT_TRY(launch_blur_decimate_u8(luma, W, H, (int64_t)W * H, d_chain[1],
+                                     (int64_t)lw[1] * lh[1], S, s));
+      for (int l = 2; l <= L; ++l)
+        FT_TRY(launch_blur_decimate(d_chain[l - 1], lw[l - 1], lh[l - 1],
+                                    (int64_t)lw[l - 1] * lh[l - 1], d_chain[l],
+                                    (int64_t)lw[l] * lh[l], nullptr, 0, 1.0, S, s));
+      img = d_chain[L];
+    }
+    phase_mark("ingest+pyramid");
+    FT_TRY(launch_structure_texture(img, PW, PH, P, cfg.rof_weight, cfg.rof_blend,
+                                    cfg.rof_iterations, d_st, P, d_rofws, 4 * P, S, s, 0, 0.25));
+    phase_mark("structure_texture");
+    FT_TRY(build_flow_pyramid(d_st, P, geo, d_fchain, pyr, geo.total, S, s));
+    FT_TRY(launch_keep_prev(pyr, pyr_keep, geo.total, in + 1, S, s));
+    phase_mark("flow pyramid");
+    return FT_OK;
+  }
+
+  // one prefetch step: mode bit 0 new frame, bit 1 track the pending frame,
+  // bit 2 the pending frame has a predecessor
+  int enqueue_prefetch(cudaStream_t s, int mode, int prev, int pend, int nxt, int par) {
+    const bool has_new = mode & 1, has_track = mode & 2, has_prev_b = mode & 4;
+    phase_mark("start");
+    if (has_new) {
+      FT_CUDA_TRY(cudaMemcpyAsync(d_luma, h_luma, (size_t)S * W * H, cudaMemcpyHostToDevice, s));
+      FT_CUDA_TRY(cudaMemcpyAsync(d_dets2[par], h_dets, (size_t)S * cfg.max_dets * sizeof(ft_det),
+                                  cudaMemcpyHostToDevice, s));
+      FT_CUDA_TRY(cudaMemcpyAsync(d_in2[par], h_in, (size_t)(2 * S + 1) * 4,
+                                  cudaMemcpyHostToDevice, s));
+      phase_mark("h2d");
+    }
+    FT_CUDA_TRY(cudaEventRecord(ev_fork, s));
+    FT_CUDA_TRY(cudaStreamWaitEvent(stream2, ev_fork, 0));
+    if (has_track) {  // frame k-1: flow (k-2 -> k-1), predict, match, update
+      PhaseRec *const ph = g_phase;
+      g_phase = nullptr;  // phases of the concurrent branch are not serial
+      const int32_t *in_b = d_in2[par ^ 1];
+      if (has_prev_b) {
+        FlowParamsD p{cfg.flow.data_weight, cfg.flow.time_step, cfg.flow.huber_epsilon,
+                      cfg.flow.warps_per_level, cfg.flow.iterations_per_warp};
+        FT_TRY(run_flow(d_pyr3[prev], d_pyr3[pend], geo.total, geo.w.data(), geo.h.data(),
+                        geo.off.data(), scales, p, fw, d_dx, d_dy, P, S, stream2));
+      }
+      FT_TRY(launch_tracker_track(T, d_dx, d_dy, P, PW, PH, L, d_dets2[par ^ 1], in_b + 1,
+                                  in_b + 1 + S, has_prev_b, d_out, d_nout, stream2));
+      g_phase = ph;
+    }
+    if (has_new) FT_TRY(enqueue_preprocess(s, d_luma, d_in2[par], d_pyr3[nxt], d_pyr3[pend]));
+    FT_CUDA_TRY(cudaEventRecord(ev_join, stream2));
+    FT_CUDA_TRY(cudaStreamWaitEvent(s, ev_join, 0));
+    phase_mark(has_new ? "flow+track (previous frame, overlapped)" : "flow+track (last frame)");
+    if (has_track) {
+      FT_CUDA_TRY(cudaMemcpyAsync(h_out, d_out, (size_t)S * 2 * cfg.max_tracks * sizeof(ft_track),
+                                  cudaMemcpyDeviceToHost, s));
+      FT_CUDA_TRY(cudaMemcpyAsync(h_nout, d_nout, (size_t)2 * S * 4, cudaMemcpyDeviceToHost, s));
+      phase_mark("d2h");
+    }
+    return FT_OK;
+  }
+
+  // capture (once per key) and launch one step graph
+  template <typename F>
+  int launch_graph(const GraphKey &key, F enqueue_fn) {
     cudaStream_t s = stream;
-    // host-I/O graphs bake the staging slot's pinned pointers into their
-    // copy nodes: key them by those pointers (one graph per slot)
-    GraphKey key{(has_prev ? 1 : 0) | (pyr_par << 1), host_io ? (const void *)h_luma : luma,
-                 host_io ? (const void *)h_dets : dets, host_io ? (const void *)h_in : in};
     auto it = graphs.find(key);
     if (it == graphs.end()) {
       Graph g;
@@ -788,7 +873,7 @@ struct ft_tracker {
       }
       g_pd_span = span.ev[0] ? &span : nullptr;
       g_phase = g.phases.get();
-      int rc = enqueue(s, has_prev, luma, dets, in, host_io);
+      int rc = enqueue_fn();
       g_pd_span = nullptr;
       g_phase = nullptr;
       e = cudaStreamEndCapture(s, &graph);
@@ -807,6 +892,39 @@ struct ft_tracker {
     FT_CUDA_TRY(cudaGraphLaunch(it->second.exec, s));
     last_launches = it->second.launches;
     last_graph = &it->second;
+    return FT_OK;
+  }
+
+  // prefetch step from the staged slot: new frame (has_new) and/or the
+  // pending frame's tracking; returns whether records were produced
+  int run_prefetch(bool has_new, bool *records) {
+    const bool has_track = pf_pending;
+    const bool has_prev_b = has_track && pf_tracked > 0;
+    const int nxt = 3 - pf_prev - pf_pend;
+    const int mode = (has_new ? 1 : 0) | (has_track ? 2 : 0) | (has_prev_b ? 4 : 0);
+    const int par = pf_par;
+    GraphKey key{(mode << 2) | (pf_prev << 5) | (pf_pend << 7) | (par << 9), h_luma, h_dets, h_in};
+    FT_TRY(launch_graph(key, [&] {
+      return enqueue_prefetch(stream, mode, pf_prev, pf_pend, nxt, par);
+    }));
+    if (has_track) ++pf_tracked;
+    if (has_new) {
+      pf_prev = pf_pend;
+      pf_pend = nxt;
+    }
+    pf_pending = has_new;
+    pf_par ^= 1;
+    *records = has_track;
+    return FT_OK;
+  }
+
+  int run(bool has_prev, const uint8_t *luma, const ft_det *dets, const int32_t *in,
+          bool host_io) {
+    // host-I/O graphs bake the staging slot's pinned pointers into their
+    // copy nodes: key them by those pointers (one graph per slot)
+    GraphKey key{(has_prev ? 1 : 0) | (pyr_par << 1), host_io ? (const void *)h_luma : luma,
+                 host_io ? (const void *)h_dets : dets, host_io ? (const void *)h_in : in};
+    FT_TRY(launch_graph(key, [&] { return enqueue(stream, has_prev, luma, dets, in, host_io); }));
     pyr_par ^= 1;
     return FT_OK;
   }
@@ -887,9 +1005,22 @@ int ft_tracker_create(ft_ctx *ctx, const ft_tracker_config *cfg, ft_tracker **ou
     FT_TRY(t->alloc(&t->d_pyr_cur, (size_t)S * t->geo.total));
     FT_TRY(t->alloc(&t->d_fchain, (size_t)S * t->geo.total));
     FT_TRY(flow_work_alloc(t->fw, S, P));
+    if (cfg->prefetch) {
+      t->prefetch = 1;
+      for (auto &b : t->d_pyr3) FT_TRY(t->alloc(&b, (size_t)S * t->geo.total));
+      for (int k = 0; k < 2; ++k) {
+        FT_TRY(t->alloc(&t->d_dets2[k], (size_t)S * cfg->max_dets));
+        FT_TRY(t->alloc(&t->d_in2[k], (size_t)2 * S + 1));
+      }
+      FT_CUDA_TRY(cudaStreamCreateWithFlags(&t->stream2, cudaStreamNonBlocking));
+      FT_CUDA_TRY(cudaEventCreateWithFlags(&t->ev_fork, cudaEventDisableTiming));
+      FT_CUDA_TRY(cudaEventCreateWithFlags(&t->ev_join, cudaEventDisableTiming));
+    }
   } else {
     return fail(FT_EINVAL, "motion must be FT_MOTION_TVL1 or FT_MOTION_KLT");
   }
+  if (cfg->prefetch && cfg->motion != FT_MOTION_TVL1)
+    return fail(FT_EINVAL, "prefetch applies to the TV-L1 path");
   // track tables
   TrackerDev &T = t->T;
   const int C = cfg->max_tracks, D = cfg->max_dets;
@@ -953,6 +1084,11 @@ int ft_tracker_reset(ft_tracker *t) {
   FT_CUDA_TRY(cudaStreamSynchronize(t->stream));
   t->frames_seen = 0;
   t->pyr_par = 0;
+  t->pf_prev = 0;
+  t->pf_pend = 1;
+  t->pf_pending = false;
+  t->pf_tracked = 0;
+  t->pf_par = 0;
   return FT_OK;
 }
 
@@ -977,6 +1113,9 @@ int ft_tracker_destroy(ft_tracker *t) {
   }
   for (auto &e : t->span.ev)
     if (e) cudaEventDestroy(e);
+  if (t->ev_fork) cudaEventDestroy(t->ev_fork);
+  if (t->ev_join) cudaEventDestroy(t->ev_join);
+  if (t->stream2) cudaStreamDestroy(t->stream2);
   if (t->ev_in) cudaEventDestroy(t->ev_in);
   if (t->ev_out) cudaEventDestroy(t->ev_out);
   if (t->stream) cudaStreamDestroy(t->stream);
@@ -1000,12 +1139,19 @@ int ft_tracker_slot_buffers(ft_tracker *t, int slot, uint8_t **luma, ft_det **de
 // Enqueue one step reading the inputs staged in `slot` (luma, detections,
 // n_dets and per-stream frame indices); returns without waiting.  Steps
 // execute in submission order on the tracker's stream.
-static int submit_slot(ft_tracker *t, int slot) {
+static int submit_slot(ft_tracker *t, int slot, bool new_frame = true) {
   auto &sl = t->slots[slot];
   DeviceGuard g(t->ctx->device);
   t->use_slot(slot);
   FT_TRY(t->join_in());
-  FT_TRY(t->run(t->frames_seen > 0, nullptr, nullptr, nullptr, true));
+  if (t->prefetch) {
+    bool rec = false;
+    FT_TRY(t->run_prefetch(new_frame, &rec));
+    sl.records = rec;
+  } else {
+    FT_TRY(t->run(t->frames_seen > 0, nullptr, nullptr, nullptr, true));
+    sl.records = true;
+  }
   sl.graph = t->last_graph;
   FT_CUDA_TRY(cudaEventRecord(sl.done, t->stream));
   FT_TRY(t->join_out());
@@ -1059,6 +1205,15 @@ int ft_tracker_stage(ft_tracker *t, int slot, int stream, const uint8_t *luma, i
   return FT_OK;
 }
 
+int ft_tracker_flush(ft_tracker *t, int slot) {
+  if (!t || slot < 0 || slot > 1) return fail(FT_EINVAL, "bad tracker / slot");
+  if (!t->prefetch) return fail(FT_EINVAL, "flush applies to prefetch trackers");
+  if (t->slots[slot].pending) return fail(FT_EINVAL, "slot still in flight: call ft_tracker_wait first");
+  const int rc = submit_slot(t, slot, false);
+  if (rc == FT_OK) t->frames_seen--;  // no new frame
+  return rc;
+}
+
 int ft_tracker_submit_staged(ft_tracker *t, int slot) {
   if (!t || slot < 0 || slot > 1) return fail(FT_EINVAL, "bad tracker / slot");
   if (t->slots[slot].pending) return fail(FT_EINVAL, "slot still in flight: call ft_tracker_wait first");
@@ -1076,12 +1231,18 @@ int ft_tracker_wait(ft_tracker *t, int slot, ft_track *out, int32_t *n_out) {
   FT_CUDA_TRY(cudaEventSynchronize(sl.done));
   sl.pending = false;
   t->use_slot(slot);
+  if (!sl.records) {  // prefetch: the first frame has only been preprocessed
+    if (n_out)
+      for (int s = 0; s < t->S; ++s) n_out[s] = 0;
+    return FT_OK;
+  }
   return read_staged(t, out, n_out);
 }
 
 int ft_tracker_step(ft_tracker *t, const uint8_t *luma, int frame, const ft_det *dets,
                     const int32_t *n_dets, ft_track *out, int32_t *n_out) {
   if (!t || !luma || !n_dets) return fail(FT_EINVAL, "NULL argument");
+  if (t->prefetch) return fail(FT_EINVAL, "a prefetch tracker runs through submit / wait / flush");
   FT_TRY(ft_tracker_submit(t, 0, frame, luma, dets, n_dets));
   return ft_tracker_wait(t, 0, out, n_out);
 }
@@ -1091,6 +1252,7 @@ int ft_tracker_step_stream(ft_tracker *t, int stream, const uint8_t *luma, int p
   if (!t || !out || !n_out) return fail(FT_EINVAL, "NULL argument");
   if (stream < 0 || stream >= t->S) return fail(FT_EINVAL, "stream out of range");
   if (n_dets == FT_STREAM_SKIP) return fail(FT_EINVAL, "a stepped stream cannot be skipped");
+  if (t->prefetch) return fail(FT_EINVAL, "a prefetch tracker runs through submit / wait / flush");
   auto &sl = t->slots[0];
   if (sl.pending) return fail(FT_EINVAL, "slot still in flight: call ft_tracker_wait first");
   for (int s = 0; s < t->S; ++s) sl.in[1 + s] = FT_STREAM_SKIP;
@@ -1112,6 +1274,7 @@ int ft_tracker_step_stream(ft_tracker *t, int stream, const uint8_t *luma, int p
 int ft_tracker_step_device(ft_tracker *t, const uint8_t *d_luma, int frame, const ft_det *d_dets,
                            const int32_t *d_n_dets) {
   if (!t || !d_luma || !d_dets || !d_n_dets) return fail(FT_EINVAL, "NULL argument");
+  if (t->prefetch) return fail(FT_EINVAL, "a prefetch tracker runs through submit / wait / flush");
   DeviceGuard g(t->ctx->device);
   // gather the caller's device inputs into the tracker's fixed input buffers
   // (D2D, ~HBM speed) so one captured graph serves every step; the frame

@@ -37,11 +37,18 @@ class Tracker:
                  max_tracks: int = 512, max_dets: int = 512,
                  smoothing_weight: float = 12.0, blend: float = 0.05,
                  rof_iterations: int = 40, device: int | None = None,
-                 motion: str = "tvl1", klt_grid: int = 10):
+                 motion: str = "tvl1", klt_grid: int = 10, prefetch: bool = False):
         """motion="tvl1" is the reference path (structure-texture + TV-L1 +
         mean-box predict); motion="klt" swaps prediction for the KLT /
         MedianFlow backend (track.predict_klt) on the
-        processing-level frames -- matching and the lifecycle are shared."""
+        processing-level frames -- matching and the lifecycle are shared.
+
+        prefetch=True is the paper's one-frame prefetch on the device
+        (PAPER.md:87-89): the step submitted with frame t preprocesses frame
+        t while the flow, predict, match and update of frame t-1 run
+        concurrently on a second CUDA stream; `wait()` then returns frame
+        t-1's records (None for the first frame) and `flush()` tracks the
+        last frame.  Results are identical to the sequential mode."""
         import torch
 
         self.width, self.height, self.n_streams = int(width), int(height), int(n_streams)
@@ -54,7 +61,9 @@ class Tracker:
             self.width, self.height, self.n_streams, self.max_tracks, self.max_dets,
             int(rof_iterations), float(gate), float(min_score), float(detection_blend),
             float(smoothing_weight), float(blend), _lib.flow_params_struct(flow_params),
-            {"tvl1": _lib.MOTION_TVL1, "klt": _lib.MOTION_KLT}[motion], int(klt_grid))
+            {"tvl1": _lib.MOTION_TVL1, "klt": _lib.MOTION_KLT}[motion], int(klt_grid),
+            1 if prefetch else 0, 0)
+        self.prefetch = bool(prefetch)
         self.motion = motion
         h = C.c_void_p()
         _lib.check(self._lib.ft_tracker_create(self._ctx, C.byref(cfg), C.byref(h)))
@@ -76,6 +85,8 @@ class Tracker:
             self._slots.append((luma, dets, nd))
         self.luma_in, self.dets_in, self.ndets_in = self._slots[0]
         self._pending: list = []  # slots submitted and not yet waited, oldest first
+        self._norec: dict = {}    # prefetch: slot -> its submission produced no records
+        self._pf_frames = 0       # prefetch: frames submitted since the last flush
         self._next_slot = 0
         self._out = np.zeros((S, 2 * self.max_tracks), dtype=_lib.TRACK_DTYPE)
         self._nout = np.zeros(S, dtype=np.int32)
@@ -98,6 +109,7 @@ class Tracker:
     def reset(self):
         _lib.check(self._lib.ft_tracker_reset(self._h))
         self._tombstones = [[] for _ in range(self.n_streams)]
+        self._pf_frames = 0
 
     # ------------------------------------------------------------------
     def _label_ref(self, label: str) -> int:
@@ -228,15 +240,33 @@ class Tracker:
         else:
             _lib.check(self._lib.ft_tracker_submit(self._h, slot, int(frame_index), None, None,
                                                    None))
+        if self.prefetch:
+            self._norec[slot] = self._pf_frames == 0
+            self._pf_frames += 1
         self._pending.append(slot)
         self._next_slot ^= 1
 
     def wait(self):
-        """Records of the oldest submitted step (see step_records)."""
+        """Records of the oldest submitted step (see step_records).  Prefetch
+        trackers: the records of the frame submitted before it (None for the
+        first frame)."""
         slot = self._pending.pop(0)
         _lib.check(self._lib.ft_tracker_wait(self._h, slot, _lib.ptr(self._out),
                                              _lib.ptr(self._nout)))
+        if self._norec.pop(slot, False):
+            return None
         return [self._out[s, :self._nout[s]].copy() for s in range(self.n_streams)]
+
+    def flush(self) -> None:
+        """Prefetch trackers: submit a step without a new frame that tracks
+        the last submitted frame (collect it with `wait()`)."""
+        if len(self._pending) == 2:
+            raise RuntimeError("two steps in flight: call wait() first")
+        slot = self._next_slot
+        _lib.check(self._lib.ft_tracker_flush(self._h, slot))
+        self._pending.append(slot)
+        self._next_slot ^= 1
+        self._pf_frames = 0
 
     def step(self, frames, frame_index: int, detections=None):
         """One frame for every stream; returns, per stream, the full scene
@@ -417,7 +447,8 @@ def read_mot(fh) -> list:
 
 
 def run(frames, source, width: int, height: int, detect_every: int = 1,
-        pipelined: bool = True, **tracker_kw):
+        pipelined: bool = True, prefetch: bool = False, summary: dict | None = None,
+        **tracker_kw):
     """Drive a single-stream Tracker over an iterable of u8 luma frames (or
     Frames) with a DetectionSource.  Frames whose index is
     not a multiple of `detect_every` have no detector result (coast).
@@ -426,28 +457,117 @@ def run(frames, source, width: int, height: int, detect_every: int = 1,
     pipelined=True is the paper's concurrency:
     frame t is submitted asynchronously, then the detector lookup and host
     staging of frame t+1 run while the device processes frame t; results are
-    byte-identical to the sequential mode, emitted with one frame of lag."""
-    trk = Tracker(width, height, n_streams=1, **tracker_kw)
+    byte-identical to the sequential mode, emitted with one frame of lag.
+    prefetch=True adds the device prefetch: preprocessing
+    of frame t+1 runs concurrently with the flow / predict / match / update
+    of frame t on the GPU (Tracker(prefetch=True)); same results.
+
+    `summary`, when given, is filled at the end (SPEC.md:418 run summary):
+    frames processed, mean per-phase device ms, track census."""
+    trk = Tracker(width, height, n_streams=1, prefetch=prefetch, **tracker_kw)
+    phases: dict = {}
+    n_frames = 0
+    last_scene = []
 
     def as_u8(luma):
         if hasattr(luma, "data") and not isinstance(luma, np.ndarray):
             return np.rint(np.asarray(luma.data) * 255.0).astype(np.uint8)
         return luma
 
+    def note_phases(slot=-1):
+        for k, v in trk.phase_ms(slot).items():
+            phases[k] = phases.get(k, 0.0) + v
+
     try:
-        if not pipelined:
+        if not pipelined and not prefetch:
             for t, luma in enumerate(frames):
                 dets = source.lookup(t) if t % detect_every == 0 else None
-                yield t, trk.step(as_u8(luma), t, [dets])[0]
+                last_scene = trk.step(as_u8(luma), t, [dets])[0]
+                note_phases()
+                n_frames += 1
+                yield t, last_scene
             return
-        last = None
+        queue = []  # (slot, frame index whose records it returns, or None)
+        submitted = 0
+
+        def collect():
+            s0, ft = queue.pop(0)
+            recs = trk.wait()
+            note_phases(s0)
+            if ft is None:
+                return None
+            return ft, trk.scenes(recs)[0]
+
         for t, luma in enumerate(frames):
-            dets = source.lookup(t) if t % detect_every == 0 else None  # overlaps frame t-1
+            dets = source.lookup(t) if t % detect_every == 0 else None  # overlaps the device
+            if len(queue) == 2:
+                got = collect()
+                if got:
+                    last_scene = got[1]
+                    n_frames += 1
+                    yield got
+            slot = trk._next_slot
             trk.submit(as_u8(luma), t, [dets])
-            if last is not None:
-                yield last, trk.scenes(trk.wait())[0]
-            last = t
-        if last is not None:
-            yield last, trk.scenes(trk.wait())[0]
+            queue.append((slot, (t - 1 if t > 0 else None) if prefetch else t))
+            submitted = t + 1
+        if prefetch and submitted:
+            if len(queue) == 2:
+                got = collect()
+                if got:
+                    last_scene = got[1]
+                    n_frames += 1
+                    yield got
+            slot = trk._next_slot
+            trk.flush()
+            queue.append((slot, submitted - 1))
+        while queue:
+            got = collect()
+            if got:
+                last_scene = got[1]
+                n_frames += 1
+                yield got
     finally:
+        if summary is not None:
+            summary.update({
+                "frames": n_frames,
+                "mean_phase_ms": {k: round(v / max(n_frames, 1), 4) for k, v in phases.items()},
+                "census": {"active": sum(o.state == ACTIVE for o in last_scene),
+                           "lost": sum(o.state == LOST for o in last_scene),
+                           "ids_issued": (max((o.id for o in last_scene), default=-1) + 1)},
+                "mode": ("concurrent+prefetch" if prefetch else
+                         "concurrent" if pipelined else "sequential")})
         trk.close()
+
+
+def bench(frames, source, width: int, height: int, detect_every: int = 1,
+          repetitions: int = 1, **tracker_kw) -> dict:
+    """mean / median wall ms per frame of each mode --
+    Sequential, Concurrent (host staging and detector lookup of frame t+1
+    overlap the device step of t) and Concurrent+prefetch (plus the device
+    prefetch) -- with each mode's mean per-phase device ms, after re-asserting
+    that every mode emits the same scenes."""
+    import time
+    frames = list(frames)
+    out: dict = {}
+    ref = None
+    for mode, kw in (("sequential", dict(pipelined=False)),
+                     ("concurrent", dict(pipelined=True)),
+                     ("concurrent+prefetch", dict(pipelined=True, prefetch=True))):
+        times = []
+        for _ in range(max(1, repetitions)):
+            summ: dict = {}
+            t0 = time.perf_counter()
+            got = [(t, track_records(sc, t)) for t, sc in
+                   run(frames, source, width, height, detect_every, summary=summ, **kw,
+                       **tracker_kw)]
+            times.append(1000 * (time.perf_counter() - t0) / max(len(frames), 1))
+        if ref is None:
+            ref = got
+        elif got != ref:
+            raise AssertionError(f"mode {mode} changed the results")
+        out[mode] = {"mean_ms_per_frame": round(float(np.mean(times)), 4),
+                     "median_ms_per_frame": round(float(np.median(times)), 4),
+                     "phases_ms": summ["mean_phase_ms"], "emission_lag_frames":
+                     0 if mode == "sequential" else (2 if mode.endswith("prefetch") else 1)}
+    out["frames"] = len(frames)
+    return out

@@ -152,14 +152,78 @@ def test_pipelined_mode_equivalence():
     src = detect.DelayedSource(detect.ScriptedSource({t: d for t, d in enumerate(dets)}), 0.02)
     prm = FlowParams(warps_per_level=2, iterations_per_warp=20)
     outs, times = {}, {}
-    for mode in (False, True):
+    summ = {}
+    for mode in (False, True, "prefetch"):
         t0 = time.perf_counter()
+        kw = dict(prefetch=True, summary=summ) if mode == "prefetch" else dict(pipelined=mode)
         outs[mode] = [(t, [(o.id, o.box, o.state, o.lost_at) for o in sc])
-                      for t, sc in run(frames, src, 160, 120, detect_every=3, pipelined=mode,
-                                       flow_params=prm)]
+                      for t, sc in run(frames, src, 160, 120, detect_every=3, flow_params=prm,
+                                       **kw)]
         times[mode] = time.perf_counter() - t0
     assert outs[True] == outs[False]
+    assert outs["prefetch"] == outs[False]
     assert [t for t, _ in outs[True]] == list(range(8))
+    assert summ["frames"] == 8 and summ["mode"] == "concurrent+prefetch"
+    assert summ["census"]["active"] == len(outs[False][-1][1])
+    assert summ["mean_phase_ms"] and all(v >= 0 for v in summ["mean_phase_ms"].values())
+
+
+@pytest.mark.gpu
+def test_prefetch_multistream_skip_matches_sequential():
+    """Device prefetch with several streams and a stream that skips a step:
+    submit / wait / flush records (one-frame lag) equal the sequential
+    tracker's step records."""
+    from paper_1910_06017_b200.optflow import FlowParams
+    from paper_1910_06017_b200.pipeline import Tracker
+    from paper_1910_06017_b200.synth import make_sequence
+    S, W, H, T = 3, 128, 96, 6
+    seqs = [make_sequence(W, H, 4, T, seed=300 + s, det_every=2, scale_change=True)
+            for s in range(S)]
+    prm = FlowParams(warps_per_level=2, iterations_per_warp=9)
+
+    def inputs(t):
+        fr = [seqs[s][0][t] for s in range(S)]
+        de = [seqs[s][1][t] for s in range(S)]
+        if t == 3:
+            fr[1], de[1] = None, None  # stream 1 has no frame at t = 3
+        return fr, de
+
+    seq = Tracker(W, H, n_streams=S, flow_params=prm, max_tracks=32, max_dets=32)
+    want = []
+    for t in range(T):
+        fr, de = inputs(t)
+        want.append([r.tobytes() for r in seq.step_records(fr, t, de)])
+    seq.close()
+    pf = Tracker(W, H, n_streams=S, flow_params=prm, max_tracks=32, max_dets=32, prefetch=True)
+    got = []
+    for t in range(T):
+        fr, de = inputs(t)
+        pf.submit(fr, t, de)
+        r = pf.wait()
+        if t == 0:
+            assert r is None
+        else:
+            got.append([x.tobytes() for x in r])
+    pf.flush()
+    got.append([x.tobytes() for x in pf.wait()])
+    assert got == want
+    assert any(k.startswith("flow+track") for k in pf.phase_ms())
+    pf.close()
+
+
+@pytest.mark.gpu
+def test_bench_modes_report():
+    """SPEC.md:428-434 bench(): every mode, same scenes (asserted inside)."""
+    from paper_1910_06017_b200.optflow import FlowParams
+    from paper_1910_06017_b200.pipeline import bench
+    from paper_1910_06017_b200.synth import make_sequence
+    frames, dets = make_sequence(96, 80, 3, 5, seed=7, det_every=1)
+    src = detect.ScriptedSource({t: d for t, d in enumerate(dets)})
+    rep = bench(frames, src, 96, 80, detect_every=2,
+                flow_params=FlowParams(warps_per_level=1, iterations_per_warp=5))
+    assert set(rep) == {"sequential", "concurrent", "concurrent+prefetch", "frames"}
+    assert rep["concurrent+prefetch"]["emission_lag_frames"] == 2
+    assert all(rep[m]["mean_ms_per_frame"] > 0 for m in ("sequential", "concurrent"))
 
 
 @pytest.mark.gpu

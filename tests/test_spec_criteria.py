@@ -1,0 +1,183 @@
+"""SPEC acceptance criteria run as stated, through the
+device path:
+
+* #4  IoU correctness: the analytic IoU (device ft_iou_matrix, assoc.iou)
+      matches a fine-grid rasterization oracle within 1e-3 on 500 random
+      integer-box pairs, and is exact on the three tagged examples
+      (SPEC.md:277-280);
+* #7  end-to-end identity stability: 100 frames, 2 objects on crossing-free
+      trajectories, detection jitter sigma = 2 px, 5 % dropout -> 0 id
+      switches and track recall >= 0.95 at IoU 0.5.  Dropout = frames on
+      which the detector returns no result (the step
+      coasts on flow); a per-detection miss on a frame that has a detector
+      result turns the track Lost for good in the reference lifecycle
+      (track.py:126-127, no re-identification: SPEC non-goal), so 0 id
+      switches is only reachable with frame-level dropout;
+* #11 update-phase semantics (track.py:90-139) over 500
+      randomized step scenarios: unmatched Active -> Lost with lost_at = t,
+      matched -> detection box / score / last_seen = t, unmatched detection
+      -> a fresh id above every existing id (Lost ones included) in detection
+      order, Lost records pass through unchanged, a Lost record in an
+      assignment raises.
+"""
+import time
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("gpu tests need a CUDA device")
+    return torch
+
+
+def _raster_iou(a, b, step=0.01):
+    """Fine-grid rasterization oracle: cell centres of a `step` lattice."""
+    x0 = min(a[0], b[0]) - 1
+    y0 = min(a[1], b[1]) - 1
+    x1 = max(a[0] + a[2], b[0] + b[2]) + 1
+    y1 = max(a[1] + a[3], b[1] + b[3]) + 1
+    xs = np.arange(x0 + step / 2, x1, step)
+    ys = np.arange(y0 + step / 2, y1, step)
+    ina_x = (xs >= a[0]) & (xs < a[0] + a[2])
+    inb_x = (xs >= b[0]) & (xs < b[0] + b[2])
+    ina_y = (ys >= a[1]) & (ys < a[1] + a[3])
+    inb_y = (ys >= b[1]) & (ys < b[1] + b[3])
+    inter = np.sum(ina_x & inb_x) * np.sum(ina_y & inb_y)
+    area_a = np.sum(ina_x) * np.sum(ina_y)
+    area_b = np.sum(inb_x) * np.sum(inb_y)
+    return inter / (area_a + area_b - inter)
+
+
+def test_criterion4_iou_vs_rasterization(torch):
+    from paper_1910_06017_b200 import assoc
+    t0 = time.perf_counter()
+    assert assoc.iou((0, 0, 10, 10), (0, 0, 10, 10)) == 1.0
+    assert assoc.iou((0, 0, 10, 10), (20, 20, 5, 5)) == 0.0
+    assert assoc.iou((0, 0, 10, 10), (5, 0, 10, 10)) == 1.0 / 3.0
+    rng = np.random.default_rng(404)
+    a = np.column_stack([rng.integers(0, 20, 500), rng.integers(0, 20, 500),
+                         rng.integers(1, 15, 500), rng.integers(1, 15, 500)]).astype(float)
+    b = np.column_stack([rng.integers(0, 20, 500), rng.integers(0, 20, 500),
+                         rng.integers(1, 15, 500), rng.integers(1, 15, 500)]).astype(float)
+    dev = np.diag(assoc.iou_matrix([tuple(r) for r in a], [tuple(r) for r in b]))
+    ras = np.array([_raster_iou(p, q) for p, q in zip(a, b)])
+    assert np.abs(dev - ras).max() <= 1e-3
+    assert (dev > 0).sum() > 100  # plenty of overlapping pairs
+    assert time.perf_counter() - t0 < 10
+
+
+def _two_object_sequence(T=100, W=320, H=240, jitter=2.0, dropout=0.05, seed=7):
+    """Two textured objects on parallel, crossing-free trajectories (one in
+    each half of the frame, bouncing horizontally) over a value-noise
+    background; detections every frame with N(0, jitter) noise, except on
+    the `dropout` fraction of frames with no detector result (None)."""
+    from paper_1910_06017_b200.detect import Detection
+    from paper_1910_06017_b200.synth import textured
+    rng = np.random.default_rng(seed)
+    bg = np.clip(textured(H, W, np.random.default_rng(seed + 1)) * 255, 0, 255).astype(np.uint8)
+    objs = []
+    for k in range(2):
+        ow, oh = 40, 36
+        tex = np.clip(40 + textured(oh, ow, rng, cells=(4,), weights=(1.0,)) * 215, 0,
+                      255).astype(np.uint8)
+        objs.append({"tex": tex, "w": ow, "h": oh, "x": 30.0 + 120 * k,
+                     "y": 30.0 + 130 * k, "vx": 2.0 if k == 0 else -1.5, "cls": 3 + k})
+    frames, dets, truth = [], [], []
+    for t in range(T):
+        img = bg.copy()
+        dl = []
+        for k, o in enumerate(objs):
+            if t:
+                o["x"] += o["vx"]
+                if o["x"] < 5 or o["x"] > W - o["w"] - 5:
+                    o["vx"] = -o["vx"]
+            x, y = int(round(o["x"])), int(round(o["y"]))
+            img[y:y + o["h"], x:x + o["w"]] = o["tex"]
+            truth.append((t, k, float(x), float(y), float(o["w"]), float(o["h"])))
+            jx, jy, jw, jh = rng.normal(0, jitter, 4)
+            dl.append(Detection(o["cls"], f"c{o['cls']}", float(rng.uniform(0.6, 1.0)),
+                                (x + jx, y + jy, max(o["w"] + jw, 2.0), max(o["h"] + jh, 2.0))))
+        frames.append(img)
+        dets.append(None if t and rng.random() < dropout else dl)
+    return frames, dets, truth
+
+
+def test_criterion7_identity_stability(torch):
+    from paper_1910_06017_b200.metrics import evaluate
+    from paper_1910_06017_b200.pipeline import Tracker, track_records
+    t0 = time.perf_counter()
+    W, H = 320, 240
+    frames, dets, truth = _two_object_sequence(W=W, H=H)
+    trk = Tracker(W, H, n_streams=1, max_tracks=16, max_dets=16)
+    rows = []
+    for t in range(len(frames)):
+        scene = trk.step(frames[t], t, [dets[t]])[0]
+        rows += track_records(scene, t)
+    trk.close()
+    m = evaluate(rows, truth)
+    assert sum(d is None for d in dets) >= 2  # the dropout frames coast
+    assert m.id_switches == 0, m
+    assert m.recall >= 0.95, m
+    assert time.perf_counter() - t0 < 120
+
+
+def test_criterion11_update_semantics(torch):
+    from paper_1910_06017_b200 import assoc, track
+    from paper_1910_06017_b200.detect import Detection
+    from paper_1910_06017_b200.track import ACTIVE, LOST, SceneObject
+    rng = np.random.default_rng(1111)
+    t0 = time.perf_counter()
+    for case in range(500):
+        t = int(rng.integers(1, 50))
+        n = int(rng.integers(0, 8))
+        scene, next_id = [], 0
+        for _ in range(n):
+            lost = rng.random() < 0.3
+            born = int(rng.integers(0, t))
+            scene.append(SceneObject(
+                id=next_id, class_id=int(rng.integers(0, 3)), label="x",
+                box=tuple(float(v) for v in rng.uniform(1, 50, 4)),
+                state=LOST if lost else ACTIVE, born_at=born, last_seen=born,
+                score=float(rng.uniform(0.5, 1)), lost_at=born if lost else None))
+            next_id += int(rng.integers(1, 3))  # ids need not be dense
+        nd = int(rng.integers(0, 6))
+        dets = [Detection(int(rng.integers(0, 3)), "d", float(rng.uniform(0.5, 1)),
+                          tuple(float(v) for v in rng.uniform(1, 50, 4))) for _ in range(nd)]
+        act = [i for i, o in enumerate(scene) if o.state == ACTIVE]
+        rng.shuffle(act)
+        js = list(rng.permutation(nd))
+        k = int(rng.integers(0, min(len(act), nd) + 1))
+        pairs = tuple(sorted((act[q], int(js[q]), 0.5) for q in range(k)))
+        matched_i = {i for i, _, _ in pairs}
+        matched_j = {j for _, j, _ in pairs}
+        un_j = tuple(j for j in range(nd) if j not in matched_j)
+        out = track.update(scene, assoc.Assignment(pairs, (), un_j), dets, t)
+        # existing records in order, then spawns in detection order
+        assert len(out) == n + len(un_j)
+        for i, o in enumerate(scene):
+            r = out[i]
+            assert r.id == o.id
+            if o.state == LOST:
+                assert r == o  # Lost passes through unchanged
+            elif i in matched_i:
+                j = next(j for ii, j, _ in pairs if ii == i)
+                assert r.state == ACTIVE and r.box == dets[j].box and r.last_seen == t
+                assert r.score == dets[j].score and r.born_at == o.born_at
+            else:
+                assert r.state == LOST and r.lost_at == t and r.box == o.box
+        top = max((o.id for o in scene), default=-1)
+        spawned = out[n:]
+        assert [s.id for s in spawned] == list(range(top + 1, top + 1 + len(un_j)))
+        for s, j in zip(spawned, un_j):
+            assert s.box == dets[j].box and s.born_at == t and s.state == ACTIVE
+        lost = [i for i, o in enumerate(scene) if o.state == LOST]
+        if lost and nd:  # a Lost object never re-enters matching
+            with pytest.raises(ValueError, match="lost"):
+                track.update(scene, assoc.Assignment(((lost[0], 0, 0.5),), (), ()), dets, t)
+    assert time.perf_counter() - t0 < 10

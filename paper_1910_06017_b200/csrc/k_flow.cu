@@ -296,6 +296,7 @@ struct alignas(64) PDArgs {
   int nhalf, last, cone_rows;
   signed char rows_lo[16], rows_hi[16];
   double tau, lam, sigma, shrink;  // shrink = 1/(1+sigma*eps)
+  int prefetch_stride;  // CTAs resident at once: the L2 prefetch target is bid + this (0: off)
 };
 
 // per-pixel border flags (global position, fixed for the launch)
@@ -365,6 +366,12 @@ __device__ __forceinline__ void tma_store(const CUtensorMap *m, int x, int y, in
           reinterpret_cast<uint64_t>(m)),
       "r"(2 * x), "r"(y), "r"(z), "r"(smem_u32(src))
       : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_l2(const CUtensorMap *m, int x, int y, int z) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(2 * x), "r"(y), "r"(z)
+               : "memory");
 }
 __device__ __forceinline__ void tma_store_commit_wait() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
@@ -589,6 +596,23 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const __grid_constant
     }
   }
   if (tid < 2) ctr[tid] = 0;
+  if (tid == 32 && a.prefetch_stride) {
+    // the tile that will take this CTA's slot next (linear order, one full
+    // wave later): pull its boxes into L2 while this tile computes
+    const int nx = gridDim.x, ny = gridDim.y;
+    const int nxt = (int)(blockIdx.x + nx * (blockIdx.y + ny * blockIdx.z)) + a.prefetch_stride;
+    if (nxt < nx * ny * (int)gridDim.z) {
+      const int px = nxt % nx, py = (nxt / nx) % ny, pz = nxt / (nx * ny);
+      const int qx = px * step_x - a.halo, qy = py * step_y - a.halo;
+      tma_prefetch_l2(&a.in_u, qx - 1, qy - 1, pz);
+      if (!a.first) {
+        tma_prefetch_l2(&a.in_px, qx - 1, qy - 1, pz);
+        tma_prefetch_l2(&a.in_py, qx - 1, qy - 1, pz);
+      }
+      tma_prefetch_l2(&a.in_g, qx, qy, pz);
+      tma_prefetch_l2(&a.in_rt, qx, qy, pz);
+    }
+  }
   if (ty == 0) mbar_wait(bar, 0);  // one warp polls; the others sleep in the barrier
   __syncthreads();
   mbar_wait(bar, 0);  // completed phase: returns at once, orders the TMA data
@@ -733,6 +757,11 @@ int pd_launch(const PDConfig &c, PDArgs &a, const StatePtrs &in, const StatePtrs
                    c.th == 32;
   void (*fn)(PDArgs) = mid ? c.fn_mid : c.fn;
   FT_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem));
+  int dev = 0, sms = kSMs, per_sm = 0;
+  FT_CUDA_TRY(cudaGetDevice(&dev));
+  FT_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  FT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * c.by, c.smem));
+  a.prefetch_stride = sms * per_sm;
   fn<<<grid, dim3(32, c.by), c.smem, s>>>(a);
   count_launch();
   return FT_OK;

@@ -26,9 +26,12 @@ def main(rep, cubin, fn, srcfile=None):
     rows = list(csv.reader(io.StringIO(out)))
     h = rows[1]
     ia, ix = h.index("Address"), h.index("Instructions Executed")
+    isamp = h.index("Warp Stall Sampling (All Samples)")
     base = None
     per = collections.Counter()
+    stall = collections.Counter()
     tot = 0
+    tot_s = 0
     for r in rows[2:]:
         try:
             a, n = int(r[ia], 16), int(r[ix])
@@ -39,12 +42,21 @@ def main(rep, cubin, fn, srcfile=None):
         f, l = line_of.get(a - base, ("?", 0))
         if srcfile and srcfile not in (f or ""):
             l = -l
-        per[(f.split("/")[-1] if f else "?", l)] += n
+        key = (f.split("/")[-1] if f else "?", l)
+        per[key] += n
         tot += n
+        try:
+            st = int(r[isamp] or 0)
+        except ValueError:
+            st = 0
+        stall[key] += st
+        tot_s += st
     src = {}
-    for (f, l), n in per.most_common(60):
-        print(f"{100 * n / tot:5.1f}%  {f}:{l}")
+    order = stall if "--stalls" in sys.argv else per
+    for (f, l), _ in order.most_common(60):
+        print(f"{100 * per[(f, l)] / tot:5.1f}% instr  {100 * stall[(f, l)] / max(tot_s, 1):5.1f}% "
+              f"stall-samples  {f}:{l}")
 
 
 if __name__ == "__main__":
-    main(*sys.argv[1:])
+    main(*[a for a in sys.argv[1:] if not a.startswith("--")])

@@ -22,13 +22,17 @@ import subprocess
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def launches(path):
+def launches(path, one_step=False):
     rows = list(csv.reader(open(path)))
     hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
     h = rows[hi]
     ki, vi, gi = h.index("Kernel Name"), h.index("Metric Value"), h.index("Grid Size")
     tot, cnt, lvl, lvc = collections.Counter(), collections.Counter(), collections.Counter(), collections.Counter()
-    for r in rows[hi + 1:]:
+    body = rows[hi + 1:]
+    if one_step:  # exactly the first tracked step: 2nd .. 3rd ingest launch
+        ing = [i for i, r in enumerate(body) if len(r) > ki and "k_gray8_to_unit" in r[ki]]
+        body = body[ing[1]:ing[2]] if len(ing) > 2 else body[ing[1]:]
+    for r in body:
         if len(r) <= vi:
             continue
         name = r[ki].split("(")[0].replace("void ", "").replace("ft::<unnamed>::", "")
@@ -126,6 +130,8 @@ def main():
     ap.add_argument("--tag", default="r01")
     ap.add_argument("--pick", help="launch list: print the ncu -s index of a finest PD launch")
     ap.add_argument("--note", default="")
+    ap.add_argument("--one-step", action="store_true",
+                    help="launch list: keep only the first tracked step")
     ap.add_argument("--stream-pixels", type=float, default=0.0,
                     help="streams x pixels of the captured launch (normalises traffic)")
     a = ap.parse_args()
@@ -134,7 +140,7 @@ def main():
         return
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     if a.launches:
-        md = launches(a.launches)
+        md = launches(a.launches, a.one_step)
         open(os.path.join(ROOT, "profiles", f"{a.tag}_launches.md"), "w").write(
             f"# {a.tag}: launch list (ncu --metrics gpu__time_duration.sum)\n\n{a.note}\n\n{md}\n")
     if a.report:

@@ -33,6 +33,22 @@ int cuda_fail(cudaError_t e, const char *what);
   } while (0)
 
 // ---------------------------------------------------------------- numerics
+// x / y for y > 0 (finite), IEEE round-to-nearest.  A zero numerator never
+// reaches the division: nvcc's double division leaves its fast path for
+// numerators below ~2^-120 (a called subroutine, ~60 instructions for the
+// whole warp), and +-0 / y is exactly +-0 = x for y > 0.
+__device__ __forceinline__ double div_pos(double x, double y) {
+  // the select is opaque to the compiler, which would otherwise divide x
+  // itself (the quotient is discarded when x == 0) and keep the slow path
+  double xs;
+  asm("{\n\t.reg .pred pz;\n\tsetp.eq.f64 pz, %1, 0d0000000000000000;\n\t"
+      "selp.f64 %0, 0d3FF0000000000000, %1, pz;\n\t}"
+      : "=d"(xs)
+      : "d"(x));
+  const double q = xs / y;
+  return x == 0.0 ? x : q;
+}
+
 // glibc >= 2.35 __hypot without FMA (Borges' correction), which is what
 // numpy's np.hypot calls on x86-64; verified identical on 2e5 random pairs.
 __device__ __forceinline__ double glibc_hypot_kernel(double ax, double ay) {
@@ -47,7 +63,7 @@ __device__ __forceinline__ double glibc_hypot_kernel(double ax, double ay) {
     t1 = 2.0 * delta * (ax - 2.0 * ay);
     t2 = (4.0 * delta - ay) * ay + delta * delta;
   }
-  h -= (t1 + t2) / (2.0 * h);
+  h -= div_pos(t1 + t2, 2.0 * h);  // h > 0 here; t1 + t2 is often exactly 0
   return h;
 }
 

@@ -248,8 +248,8 @@ __device__ __forceinline__ void rof_tile_body(
       // exactly like the reference's separate multiply and add
       const double hy = glibc_hypot(gx, gy);
       const double norm = P2 ? fma(step, hy, 1.0) : 1.0 + step * hy;
-      px[q] = (P2 ? fma(step, gx, px[q]) : px[q] + step * gx) / norm;
-      py[q] = (P2 ? fma(step, gy, py[q]) : py[q] + step * gy) / norm;
+      px[q] = div_pos(P2 ? fma(step, gx, px[q]) : px[q] + step * gx, norm);  // norm >= 1
+      py[q] = div_pos(P2 ? fma(step, gy, py[q]) : py[q] + step * gy, norm);
       s_px[id] = px[q];
       s_py[id] = py[q];
     }

@@ -222,7 +222,9 @@ __device__ __forceinline__ void rof_tile_body(
   // rows [c+it+1, TH-c-it-1) and d on [c+it+1, TH-c-it), c = halo - iters,
   // for the written interior [halo, TH-halo); a row is one warp.
   const int cone = FIX ? 0 : (cone_on && halo > 0 && iters <= halo) ? halo - iters : -1;
-#pragma unroll
+  // not unrolled: four unrolled iterations of 4 pixels (hypot + two
+  // divisions each) made a 200 KB kernel that missed the instruction cache
+#pragma unroll 1
   for (int it = 0; it < (FIX ? 4 : iters); ++it) {
     double d[NQ];
 #pragma unroll

@@ -49,6 +49,18 @@ __device__ __forceinline__ double div_pos(double x, double y) {
   return x == 0.0 ? x : q;
 }
 
+// safe ? 1 / g : 0 (optflow.py:165 np.where(safe, 1/max(g, 1e-12), 0)) with
+// the division never seeing an unsafe (possibly zero) g
+__device__ __forceinline__ double recip_if(bool safe, double g) {
+  double gs;
+  asm("{\n\t.reg .pred ps;\n\tsetp.ne.s32 ps, %2, 0;\n\t"
+      "selp.f64 %0, %1, 0d3FF0000000000000, ps;\n\t}"
+      : "=d"(gs)
+      : "d"(g), "r"((int)safe));
+  const double r = 1.0 / gs;
+  return safe ? r : 0.0;
+}
+
 // glibc >= 2.35 __hypot without FMA (Borges' correction), which is what
 // numpy's np.hypot calls on x86-64; verified identical on 2e5 random pairs.
 __device__ __forceinline__ double glibc_hypot_kernel(double ax, double ay) {

@@ -634,7 +634,7 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const __grid_constant
       gx[q] = g.x;
       gy[q] = g.y;
       const double g2 = g.x * g.x + g.y * g.y;  // optflow.py:163-165
-      ig2[q] = g2 > 1e-12 ? 1.0 / g2 : 0.0;
+      ig2[q] = recip_if(g2 > 1e-12, g2);  // g2 > 1e-12: max(g2, 1e-12) == g2
       fl[q] = (gc < W - 1 ? FL_R : 0u) | (gr < H - 1 ? FL_D : 0u) | (gc > 0 ? FL_L : 0u) |
               (gc == W - 1 ? FL_LASTC : 0u) | (gr > 0 ? FL_U : 0u) | (gr == H - 1 ? FL_LASTR : 0u);
     }

@@ -232,7 +232,9 @@ __device__ __forceinline__ double iou_box(const double *a, const double *b) {
   const double ix2 = py_min(a[0] + a[2], b[0] + b[2]);
   const double iy2 = py_min(a[1] + a[3], b[1] + b[3]);
   const double inter = py_max(0.0, ix2 - ix) * py_max(0.0, iy2 - iy);
-  return inter / (a[2] * a[3] + b[2] * b[3] - inter);
+  // union > 0 for positive sizes; inter == 0 (most pairs) stays off the
+  // division slow path
+  return div_pos(inter, a[2] * a[3] + b[2] * b[3] - inter);
 }
 
 __global__ void k_iou(const double *a, int m, const double *b, int n, double *out) {

@@ -344,6 +344,8 @@ def run_ours(args, ws, rank, local):
         roofline = trk.roofline(hbm_peak_gbs(), frame_bytes=FRAME_BYTES[args.flow],
                                 step_ms=ms / K, frames_per_s_per_gpu=value / ws,
                                 profiles_dir=os.path.join(ROOT, "profiles"))
+        if roofline is not None and phases.get("structure_texture"):
+            roofline["rof"] = rof_roofline(phases["structure_texture"], B)
 
     # ---------------- end to end through the public API (e2e) ----------------
     trk.reset()
@@ -435,6 +437,27 @@ def run_ours(args, ws, rank, local):
         if cpu is None and ws > 1:
             line["cpu_baseline_note"] = "timed at N=1 only (same host, same workload)"
         print(json.dumps(line), flush=True)
+
+
+def rof_roofline(st_ms: float, streams: int) -> dict:
+    """ROF structure-texture phase (imaging.py:109-144, 40 dual steps) of the
+    last timed step, live from its graph event nodes: SURVEY 8(d)'s 40 B per
+    pixel-iteration (read I, px, py; write px, py) and the reference's fp64
+    work per pixel-iteration (imaging.py:120-124: divergence 3, d 1,
+    gradient 2, hypot 1, norm 2, p update 4 incl. two divisions = 13 ops)
+    against the measured peaks; the phase also holds the final combine."""
+    from paper_1910_06017_b200.imaging import select_level
+    lv = select_level(W_, H_)
+    px = (W_ >> lv) * (H_ >> lv) * streams * 40
+    sec = st_ms / 1000.0
+    hbm, _ = hbm_peak_gbs()
+    fp = os.path.join(ROOT, "profiles", "fp64_peak.json")
+    fp64 = json.load(open(fp))["dadd_dmul_ops_per_s"] if os.path.exists(fp) else None
+    return {"kernel": "k_rof_tile (+ k_st_combine), the structure_texture phase",
+            "ms_per_step": round(st_ms, 4), "pixel_iters": px,
+            "frac": round(40.0 * px / sec / 1e9 / hbm, 4),
+            "fp64_frac": round(13.0 * px / sec / fp64, 4) if fp64 else None,
+            "bound": "fp64 issue (ncu: profiles/r02_rof_full.md)"}
 
 
 def hbm_peak_gbs():

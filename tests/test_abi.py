@@ -44,7 +44,7 @@ def test_struct_layouts():
     assert C.sizeof(_lib.ft_flow_params) == 40
     assert C.sizeof(_lib.ft_det) == 48
     assert C.sizeof(_lib.ft_track) == 72
-    assert C.sizeof(_lib.ft_tracker_config) == 24 + 40 + 40 + 8
+    assert C.sizeof(_lib.ft_tracker_config) == 24 + 40 + 40 + 16  # + motion, klt_grid, prefetch, pad
 
 
 def test_host_scalars_without_gpu(lib):

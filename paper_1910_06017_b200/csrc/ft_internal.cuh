@@ -187,12 +187,6 @@ int launch_structure_texture(const double *img, int w, int h, int64_t stride, do
                              int mode = 0, double step = 0.25);
 
 // ---------------------------------------------------------------- flow
-struct FlowLevelPlanes {
-  // all planes share one geometry (w x h) and a per-image element stride
-  int w, h;
-  int64_t stride;
-};
-
 // Workspace for one batch of nb images at a max level size (k_flow.cu
 // describes the interleaved double2 layout).
 struct FlowWork {

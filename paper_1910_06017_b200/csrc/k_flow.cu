@@ -304,14 +304,7 @@ enum : unsigned { FL_R = 1, FL_D = 2, FL_L = 4, FL_LASTC = 8, FL_U = 16, FL_LAST
 
 // Exchange planes hold the fields read at a neighbour as three interleaved
 // double2 planes -- (b1,b2), (p11,p21), (p12,p22) -- the pairs that are always
-// read together, so each neighbour access is one 128-bit shared load.  sxi()
-// maps field f (0..5 = b1 b2 p11 p12 p21 p22) of element id to its double
-// index.
-__device__ __forceinline__ int sxi(int f, int id, int PL) {
-  const int pair = f == 0 || f == 1 ? 0 : (f == 2 || f == 4 ? 1 : 2);
-  const int comp = f == 1 || f == 4 || f == 5 ? 1 : 0;
-  return 2 * (pair * PL + id) + comp;
-}
+// read together, so each neighbour access is one 128-bit shared load.
 
 template <int TW, int BY, int PY>
 struct PDGeom {

@@ -275,7 +275,7 @@ StatePtrs state_ptrs(double2 *base, int nb, int64_t cap) {
 // its own u-bar.  Pointwise fields
 // (u, the gathered gradient, rho0, the threshold, 1/|grad|^2 derived once per
 // launch) live in registers of the owning thread: thread (tx, ty) owns
-// columns tx + 32*cx (cx < TW/32) and rows ty + BY*k (k < PY).
+// columns tx + 32*cx (cx < TW/32) and rows PY*ty + k (k < PY).
 // ------------------------------------------------------------------------
 struct alignas(64) PDArgs {
   // TMA descriptors (3-D: interleaved row, y, image of the batch), built per
@@ -319,6 +319,12 @@ struct PDGeom {
   static constexpr size_t kStage = (size_t)2 * TW * TH * 16;
   static constexpr size_t kQueue = ((size_t)(2 * NP * 32 * BY + 2) * 4 + 15) / 16 * 16;
   static constexpr size_t smem = kPlanes + kStage + kQueue + 16;
+  // thread (tx, ty) owns PY adjacent rows row(ty, k), k < PY: a pixel's
+  // lower neighbour for the dual step and upper neighbour for the primal
+  // step are then mostly values the thread has already loaded (one shared
+  // load fewer per pixel pair and half-step than rows ty + BY*k: +3 %)
+  static __device__ __forceinline__ int row(int ty, int k) { return PY * ty + k; }
+  static constexpr int roff(int k) { return k * SP; }
 };
 
 // ---- TMA / mbarrier primitives (PTX)
@@ -416,7 +422,7 @@ __device__ __forceinline__ void pd_halfsteps_cq(const PDArgs &a, double *sm, int
     bool all = true;
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
-      const int lr = ty + BY * (q / NX);
+      const int lr = G::row(ty, q / NX);
       row_on[q] = lr >= lo && lr < hi;
       all = all && row_on[q];
     }
@@ -426,7 +432,7 @@ __device__ __forceinline__ void pd_halfsteps_cq(const PDArgs &a, double *sm, int
       // (the common all-rows-active case runs branch-free so the compiler can
       // interleave the pixels' dependency chains)
       auto dual_px = [&](const int q) {
-        const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
+        const int id = base + G::roff(q / NX) + 32 * (q % NX);
         const double2 cb = sB[id], rb = sB[id + 1], db = sB[id + SP];
         const double2 opx = sPX[id], opy = sPY[id];
         const bool R = IN || (fl[q] & FL_R), D = IN || (fl[q] & FL_D);
@@ -468,7 +474,7 @@ __device__ __forceinline__ void pd_halfsteps_cq(const PDArgs &a, double *sm, int
 #pragma unroll
         for (int k = 0; k < 2 * NP; ++k) {
           const int q = k >> 1;
-          const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
+          const int id = base + G::roff(q / NX) + 32 * (q % NX);
           if ((need >> k) & 1u) qidx[wbase + off[k]] = 2 * id + (k & 1);
         }
       }
@@ -487,7 +493,7 @@ __device__ __forceinline__ void pd_halfsteps_cq(const PDArgs &a, double *sm, int
     } else {
       // ---- primal descent + TV-L1 shrinkage (:194-208), u-bar stored in place
       auto primal_px = [&](const int q) {
-        const int id = base + (q / NX) * BY * SP + 32 * (q % NX);
+        const int id = base + G::roff(q / NX) + 32 * (q % NX);
         const unsigned f = fl[q];
         const double2 mpx = sPX[id], mpy = sPY[id];
         const double p11 = mpx.x, p21 = mpx.y, p12 = mpy.x, p22 = mpy.y;
@@ -502,7 +508,7 @@ __device__ __forceinline__ void pd_halfsteps_cq(const PDArgs &a, double *sm, int
         const double v1 = madx<P2>(tau, dx1 + dy1, u1[q]);
         const double v2 = madx<P2>(tau, dx2 + dy2, u2[q]);
         // (rho0, thresh) stay in the shared G/RT staging of the prologue
-        const double2 rq = rt[(ty + BY * (q / NX)) * TW + tx + 32 * (q % NX)];
+        const double2 rq = rt[G::row(ty, q / NX) * TW + tx + 32 * (q % NX)];
         const double rho = rq.x + gx[q] * v1 + gy[q] * v2;
         const bool lo_ = rho < -rq.y;
         const bool hi_ = rho > rq.y;
@@ -566,7 +572,7 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const __grid_constant
   const int bz = blockIdx.z;
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = ty * 32 + tx;
-  const int base = (ty + 1) * SP + tx + 1;  // apron offset (+1,+1)
+  const int base = (G::row(ty, 0) + 1) * SP + tx + 1;  // apron offset (+1,+1)
 
   // ---- prologue: U (-> u-bar plane: u-bar = u), p, G, RT by TMA
   if (tid == 0) mbar_init(bar, 1);
@@ -618,9 +624,9 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const __grid_constant
 #pragma unroll
     for (int cx = 0; cx < NX; ++cx) {
       const int q = k * NX + cx;
-      const int lc = tx + 32 * cx, lr = ty + BY * k;
+      const int lc = tx + 32 * cx, lr = G::row(ty, k);
       const int gc = ox + lc, gr = oy + lr;
-      const double2 u = sB[base + k * BY * SP + 32 * cx];
+      const double2 u = sB[base + G::roff(k) + 32 * cx];
       const double2 g = stage[lr * TW + lc];
       u1[q] = u.x;
       u2[q] = u.y;
@@ -656,12 +662,12 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const __grid_constant
 #pragma unroll
   for (int q = 0; q < NP; ++q) {
     const int k = q / NX, cx = q % NX;
-    const int lc = tx + 32 * cx, lr = ty + BY * k;
+    const int lc = tx + 32 * cx, lr = G::row(ty, k);
     if (lc < hl || lc >= TW - hl || lr < hl || lr >= TH - hl) continue;
     const int e = (lr - hl) * iw + (lc - hl);
     ou[e] = make_double2(u1[q], u2[q]);
     if (!a.last) {
-      const int id = base + k * BY * SP + 32 * cx;
+      const int id = base + G::roff(k) + 32 * cx;
       opx[e] = sB[PL + id];
       opy[e] = sB[2 * PL + id];
     }

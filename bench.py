@@ -348,24 +348,32 @@ def run_ours(args, ws, rank, local):
             roofline["rof"] = rof_roofline(phases["structure_texture"], B)
 
     # ---------------- end to end through the public API (e2e) ----------------
-    trk.reset()
     recs = [[dets[t, s][:max(ndets[t, s], 0)] if ndets[t, s] >= 0 else None for s in range(B)]
             for t in range(T)]
-    for t in range(Wm + 1):
-        trk.step_records(frames[t], t, recs[t])
-    torch.cuda.synchronize(dev)
-    barrier(ws)
-    t0 = time.perf_counter()
-    last = None
-    # pipelined public API: stage + submit frame t, then collect frame t-1
-    # (each step still does its own pinned H2D and D2H inside the region)
-    for t in range(Wm + 1, T):
-        trk.submit(frames[t], t, recs[t])
-        if t > Wm + 1:
-            last = trk.wait()
-    last = trk.wait()
-    torch.cuda.synchronize(dev)
-    e2e_s = allmax(ws, time.perf_counter() - t0)
+
+    def e2e_pass():
+        trk.reset()
+        for t in range(Wm + 1):
+            trk.step_records(frames[t], t, recs[t])
+        torch.cuda.synchronize(dev)
+        barrier(ws)
+        t0 = time.perf_counter()
+        last = None
+        # pipelined public API: stage + submit frame t, then collect frame t-1
+        # (each step still does its own pinned H2D and D2H inside the region)
+        for t in range(Wm + 1, T):
+            trk.submit(frames[t], t, recs[t])
+            if t > Wm + 1:
+                last = trk.wait()
+        last = trk.wait()
+        torch.cuda.synchronize(dev)
+        return time.perf_counter() - t0, last
+
+    # an untimed pass first: the step graphs of the pipelined slots are
+    # captured there, not inside the timed region
+    e2e_pass()
+    e2e_s, last = e2e_pass()
+    e2e_s = allmax(ws, e2e_s)
     barrier(ws)
     total_frames = ws * B * K if args.total_streams is None else args.total_streams * K
     e2e = total_frames / e2e_s
@@ -389,6 +397,15 @@ def run_ours(args, ws, rank, local):
         # overlaps flow/predict/match/update of frame t on the device
         pf = Tracker(W_, H_, n_streams=B, flow_params=prm, max_tracks=max_tracks,
                      max_dets=max_dets, device=local, prefetch=True)
+        # one untimed pass captures every step graph the rotation uses (new
+        # frame / pending frame / three pyramid buffers / input parity: six
+        # in the steady state), then the timed pass replays them
+        for t in range(T):
+            pf.submit(frames[t], t, recs[t])
+            if t:
+                pf.wait()
+        pf.wait()
+        pf.reset()
         for t in range(Wm + 1):
             pf.submit(frames[t], t, recs[t])
             pf.wait()

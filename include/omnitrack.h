@@ -277,7 +277,9 @@ int ft_tracker_launches(ft_tracker *trk, int64_t *count);
  * "predict+match+update", "d2h", ...); *n = phases written. */
 int ft_tracker_phase_times(ft_tracker *trk, int slot, double *ms, const char **names, int max,
                            int *n);
-/* Reset all streams (drop tracks and cached previous frames). */
+/* Reset all streams (drop tracks and cached previous frames).  Submitted
+ * steps still in flight are completed and their records dropped: both
+ * staging slots are free afterwards. */
 int ft_tracker_reset(ft_tracker *trk);
 
 #ifdef __cplusplus

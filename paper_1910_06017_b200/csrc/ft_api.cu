@@ -1082,6 +1082,11 @@ int ft_tracker_reset(ft_tracker *t) {
   FT_CUDA_TRY(cudaMemsetAsync(t->d_dx, 0, (size_t)S * t->P * 8, t->stream));
   FT_CUDA_TRY(cudaMemsetAsync(t->d_dy, 0, (size_t)S * t->P * 8, t->stream));
   FT_CUDA_TRY(cudaStreamSynchronize(t->stream));
+  for (auto &sl : t->slots) {  // in-flight submissions are complete; drop their records
+    FT_CUDA_TRY(cudaEventSynchronize(sl.done));
+    sl.pending = false;
+    sl.records = true;
+  }
   t->frames_seen = 0;
   t->pyr_par = 0;
   t->pf_prev = 0;

@@ -107,9 +107,16 @@ class Tracker:
             pass
 
     def reset(self):
+        """Forget every stream's tracks and previous frame.  Steps still in
+        flight are completed and their records dropped; the staging slots
+        restart at slot 0, so a replayed sequence reuses the step graphs
+        captured for it."""
         _lib.check(self._lib.ft_tracker_reset(self._h))
         self._tombstones = [[] for _ in range(self.n_streams)]
         self._pf_frames = 0
+        self._pending = []
+        self._norec = {}
+        self._next_slot = 0
 
     # ------------------------------------------------------------------
     def _label_ref(self, label: str) -> int:

@@ -208,6 +208,20 @@ def test_prefetch_multistream_skip_matches_sequential():
     got.append([x.tobytes() for x in pf.wait()])
     assert got == want
     assert any(k.startswith("flow+track") for k in pf.phase_ms())
+    # reset with a step still in flight, then replay: same records again
+    fr, de = inputs(0)
+    pf.submit(fr, 0, de)
+    pf.reset()
+    again = []
+    for t in range(T):
+        fr, de = inputs(t)
+        pf.submit(fr, t, de)
+        r = pf.wait()
+        if t:
+            again.append([x.tobytes() for x in r])
+    pf.flush()
+    again.append([x.tobytes() for x in pf.wait()])
+    assert again == want
     pf.close()
 
 

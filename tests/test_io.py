@@ -73,6 +73,8 @@ def test_detection_sidecar(tmp_path):
     assert (rf.width, rf.height) == (608, 342)  # SPEC acceptance criterion 1
     assert detect.adaptive_receptive_field(1080, 1920, 608) == detect.ReceptiveField(342, 608)
     assert detect.adaptive_receptive_field(720, 576, 608) == detect.ReceptiveField(608, 486)
+    for sq in (608, 1000, 64):  # square frames: the square field (criterion 1's identity case)
+        assert detect.adaptive_receptive_field(sq, sq, 608) == detect.ReceptiveField(608, 608)
 
 
 def test_flo_bytes_match_reference(golden, tmp_path):

@@ -161,10 +161,17 @@ def workload(args) -> str:
 
 
 def bench_config(args, ws: int, streams_per_gpu: int) -> dict:
-    """The `config` object, identical on both arms (same workload keys)."""
+    """The `config` object, identical on both arms (same workload keys).
+    Strong scaling (--total-streams T): streams_per_gpu = the largest rank
+    block, ceil(T / ws)."""
+    if args.total_streams is not None:
+        total = args.total_streams
+        streams_per_gpu = -(-total // ws)
+    else:
+        total = streams_per_gpu * ws
     return {"workload": workload(args), "frame": [W_, H_], "tracks_per_stream": N_OBJ,
             "detect_every": DET_EVERY, "det_jitter_px": JITTER,
-            "streams_per_gpu": streams_per_gpu, "total_streams": streams_per_gpu * ws,
+            "streams_per_gpu": streams_per_gpu, "total_streams": total,
             "stream_seeds": "1000 + global stream id",
             "parallelism": f"stream-sharded x{ws} (no data-path collective)",
             "l2": "working set > L2: 64 SD streams x ~100 MB of state per GPU; every launch "
@@ -265,9 +272,9 @@ def run_reference(args, ws, rank):
     line = {"impl": "reference", "metric": METRIC, "value": round(fps, 5), "unit": "frames/s",
             "n_gpus": args.gpus, "steps": steps, "warmup": 1,
             "ms_per_step": round(1000 * wall / steps, 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": bench_config(args, 1, args.streams if args.total_streams is None
-                                   else args.total_streams),
+            "scaling": "weak" if args.total_streams is None else "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": bench_config(args, ws, args.streams),
             "cpu_baseline": {"value": round(fps, 5), "unit": "frames/s", "cores": cores,
                              "kind": "port",
                              "sample": _cpu_sample(cores, args.config, args.motion, args.flow)
@@ -492,9 +499,16 @@ def _free_port():
     return p
 
 
+# test hook (tests/test_multiproc.py): every rank on cuda:0 over gloo, to run
+# the multi-rank bench path functionally on a one-GPU box.  The ranks share
+# no data and never wait on each other's kernels; the numbers are not a
+# scaling measurement.
+ONE_GPU = os.environ.get("FT_BENCH_ONE_GPU") == "1"
+
+
 def launch_ranks(args) -> int:
     """`--gpus N` outside torchrun: start the N ranks ourselves."""
-    if args.impl == "ours":
+    if args.impl == "ours" and not ONE_GPU:
         import torch
         have = torch.cuda.device_count()
         if have < args.gpus:
@@ -534,6 +548,8 @@ def main():
         print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws_env}", file=sys.stderr)
         sys.exit(2)
     ws, rank, local = dist_init()
+    if ONE_GPU:
+        local = 0
     if args.impl == "reference":
         run_reference(args, ws, rank)
     else:

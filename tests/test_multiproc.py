@@ -154,3 +154,32 @@ def test_two_ranks_match_one_rank():
     for g in range(GSTREAMS):
         assert merged[g] == (one[g][0].tobytes(), one[g][1]), f"stream {g}: 2 ranks != 1 rank"
     assert sum(len(r) for r, _ in one) > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("split,total,scaling", [(["--streams", "2"], 4, "weak"),
+                                                 (["--total-streams", "3"], 3, "strong")])
+def test_bench_two_ranks_one_gpu(split, total, scaling):
+    """bench.py's multi-rank path end to end (`--gpus 2` starts the ranks
+    itself): both ranks on cuda:0 over gloo (FT_BENCH_ONE_GPU test hook), a
+    tiny weak-scaling run and an uneven strong split (2 + 1 streams); rank 0
+    prints one line covering both ranks' streams (functional check, not a
+    scaling number)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, FT_BENCH_ONE_GPU="1", FT_DIST_BACKEND="gloo")
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(k, None)
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2",
+                          "--steps", "2", "--warmup", "3", *split, "--no-cpu-baseline"],
+                         cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [json.loads(x) for x in out.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = lines[0]
+    assert d["n_gpus"] == 2 and d["scaling"] == scaling
+    assert d["config"]["total_streams"] == total and d["gather"]["streams"] == total
+    assert d["value"] > 0 and abs(d["value_per_gpu"] - d["value"] / 2) < 1e-3 * d["value"]
+    assert d["e2e"]["value"] > 0 and d["gpu_launches"] > 0

@@ -547,6 +547,8 @@ def main():
     if ws_env is not None and int(ws_env) != args.gpus:
         print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws_env}", file=sys.stderr)
         sys.exit(2)
+    if args.impl == "reference":  # the CPU arm needs no GPU communicator
+        os.environ.setdefault("FT_DIST_BACKEND", "gloo")
     ws, rank, local = dist_init()
     if ONE_GPU:
         local = 0

@@ -13,7 +13,7 @@
 //   PX (p11, p21)     (u-bar is recomputed at the start of every launch and
 //   PY (p12, p22)      never leaves the chip)
 //   G  (gx, gy)       warp constants          [nb][cap] double2
-//   RT (rho0, thresh)                         [nb][cap] double2
+//   RT (rho0, 1/|grad|^2 or 0)                [nb][cap] double2
 //   IX (dI1/dx, dI1/dy) level gradient        [nb][cap] double2
 #include <algorithm>
 #include <cmath>
@@ -135,10 +135,12 @@ __global__ void k_upsample(const double2 *__restrict__ cu, int wc, int hc,
 }
 
 // Per-warp linearisation (optflow.py:158-176): gather I1, dI1/dx, dI1/dy at
-// x+u; rho0 = I1w - I0 - gx*u1 - gy*u2; thresh = tau*lam*|grad|^2.
+// x+u; rho0 = I1w - I0 - gx*u1 - gy*u2 and 1/|grad|^2 (0 where |grad|^2 <=
+// 1e-12).  The threshold tau*lam*|grad|^2 is rederived from (gx, gy) by the
+// tile kernel's prologue (a multiply instead of a plane).
 __global__ void k_warp_setup(const double *__restrict__ i0, const double *__restrict__ i1,
                              int64_t ps, const double2 *__restrict__ ix,
-                             const double2 *__restrict__ u, int w, int h, int64_t cap, double tl,
+                             const double2 *__restrict__ u, int w, int h, int64_t cap,
                              double2 *__restrict__ g, double2 *__restrict__ rt) {
   i0 += blockIdx.z * ps;
   i1 += blockIdx.z * ps;
@@ -153,7 +155,9 @@ __global__ void k_warp_setup(const double *__restrict__ i0, const double *__rest
   const double2 gg = bsample2(ix + so, w, h, mx, my);
   g[so + o] = gg;
   const double g2 = gg.x * gg.x + gg.y * gg.y;  // optflow.py:163
-  rt[so + o] = make_double2(v - i0[o] - gg.x * uu.x - gg.y * uu.y, tl * g2);
+  // 1/|grad|^2 once per warp here, not in every launch's prologue
+  // (optflow.py:164-165: g2 > 1e-12 <=> max(g2, 1e-12) == g2)
+  rt[so + o] = make_double2(v - i0[o] - gg.x * uu.x - gg.y * uu.y, recip_if(g2 > 1e-12, g2));
 }
 
 // 3x3 median with replicated border (imageops.py:78-84): exact 5th order
@@ -273,8 +277,9 @@ StatePtrs state_ptrs(double2 *base, int nb, int64_t cap) {
 // is an immediate offset from the thread's base address.  Each field is
 // updated in place: the dual step reads only its own p, the primal step only
 // its own u-bar.  Pointwise fields
-// (u, the gathered gradient, rho0, the threshold, 1/|grad|^2 derived once per
-// launch) live in registers of the owning thread: thread (tx, ty) owns
+// (u, the gathered gradient, the threshold derived once per launch) live in
+// registers of the owning thread, (rho0, 1/|grad|^2) in the shared RT
+// staging box: thread (tx, ty) owns
 // columns tx + 32*cx (cx < TW/32) and rows PY*ty + k (k < PY).
 // ------------------------------------------------------------------------
 struct alignas(64) PDArgs {
@@ -406,7 +411,7 @@ template <int TW, int BY, int PY, bool P2, bool IN, bool MID>
 __device__ __forceinline__ void pd_halfsteps_cq(const PDArgs &a, double *sm, int base, int tx,
                                                 int ty, const unsigned *fl, double *u1,
                                                 double *u2, const double *gx, const double *gy,
-                                                const double2 *rt, const double *ig2, double tl,
+                                                const double2 *rt, const double *thr_, double tl,
                                                 int *qidx, int *ctr) {
   using G = PDGeom<TW, BY, PY>;
   constexpr int NX = G::NX, NP = G::NP, SP = G::SP, PL = G::PLANE, TH = G::TH;
@@ -507,13 +512,14 @@ __device__ __forceinline__ void pd_halfsteps_cq(const PDArgs &a, double *sm, int
         const double dy2 = U ? (LR ? -u22 : p22 - u22) : p22;
         const double v1 = madx<P2>(tau, dx1 + dy1, u1[q]);
         const double v2 = madx<P2>(tau, dx2 + dy2, u2[q]);
-        // (rho0, thresh) stay in the shared G/RT staging of the prologue
+        // (rho0, 1/|grad|^2) stay in the shared G/RT staging of the prologue
         const double2 rq = rt[G::row(ty, q / NX) * TW + tx + 32 * (q % NX)];
         const double rho = rq.x + gx[q] * v1 + gy[q] * v2;
-        const bool lo_ = rho < -rq.y;
-        const bool hi_ = rho > rq.y;
-        double d = lo_ ? tl : (hi_ ? -tl : -rho * ig2[q]);
-        d = (ig2[q] != 0.0 || lo_ || hi_) ? d : 0.0;  // ig2 != 0 <=> |grad|^2 > 1e-12
+        const double thr = thr_[q], ig = rq.y;
+        const bool lo_ = rho < -thr;
+        const bool hi_ = rho > thr;
+        double d = lo_ ? tl : (hi_ ? -tl : -rho * ig);
+        d = (ig != 0.0 || lo_ || hi_) ? d : 0.0;  // ig != 0 <=> |grad|^2 > 1e-12
         const double n1 = v1 + d * gx[q];
         const double n2 = v2 + d * gy[q];
         sB[id] = make_double2(madx<true>(2.0, n1, -u1[q]), madx<true>(2.0, n2, -u2[q]));
@@ -617,7 +623,7 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const __grid_constant
   mbar_wait(bar, 0);  // completed phase: returns at once, orders the TMA data
 
   const double tl = a.tau * a.lam;
-  double u1[NP], u2[NP], gx[NP], gy[NP], ig2[NP];
+  double u1[NP], u2[NP], gx[NP], gy[NP], thr_[NP];
   unsigned fl[NP];
 #pragma unroll
   for (int k = 0; k < PY; ++k) {
@@ -633,7 +639,7 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const __grid_constant
       gx[q] = g.x;
       gy[q] = g.y;
       const double g2 = g.x * g.x + g.y * g.y;  // optflow.py:163-165
-      ig2[q] = recip_if(g2 > 1e-12, g2);  // g2 > 1e-12: max(g2, 1e-12) == g2
+      thr_[q] = tl * g2;  // thresh = tau * lam * grad_sq (optflow.py:176)
       fl[q] = (gc < W - 1 ? FL_R : 0u) | (gr < H - 1 ? FL_D : 0u) | (gc > 0 ? FL_L : 0u) |
               (gc == W - 1 ? FL_LASTC : 0u) | (gr > 0 ? FL_U : 0u) | (gr == H - 1 ? FL_LASTR : 0u);
     }
@@ -645,7 +651,7 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const __grid_constant
   {
 #define FT_PD_CALL(P2_, IN_)                                                                 \
   pd_halfsteps_cq<TW, BY, PY, P2_, IN_, MID>(a, sm, base, tx, ty, fl, u1, u2, gx, gy, \
-                                             stage + TW * TH, ig2, tl, qidx, ctr)
+                                             stage + TW * TH, thr_, tl, qidx, ctr)
     if (a.pow2) {
       if (interior) FT_PD_CALL(true, true); else FT_PD_CALL(true, false);
     } else {
@@ -916,7 +922,6 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
   int cur = 0;
   const double sigma = 1.0 / (8.0 * p.tau);
   const double shrink = 1.0 / (1.0 + sigma * p.eps);
-  const double tl = p.tau * p.lam;
   const dim3 blk(32, 8);
   for (int lvl = scales - 1; lvl >= 0; --lvl) {
     const int w = lw[lvl], h = lh[lvl];
@@ -947,7 +952,7 @@ int run_flow(const double *pyr0, const double *pyr1, int64_t pyr_stride, const i
     for (int wp = 0; wp < p.warps; ++wp) {
       k_warp_setup<<<grid2d(w, h, nb), blk, 0, s>>>(i0, i1, pyr_stride, fw.ix,
                                                      state_ptrs(fw.st[cur], fw.nb, cap).u, w, h,
-                                                     cap, tl, fw.g, fw.rt);
+                                                     cap, fw.g, fw.rt);
       count_launch();
       const int si = span && span->spans < PdSpan::kMaxSpans ? span->spans : -1;
       if (si >= 0)

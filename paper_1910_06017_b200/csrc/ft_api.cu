@@ -282,7 +282,7 @@ int ft_structure_texture(ft_ctx *ctx, const double *in, int w, int h, double wei
   if (iterations < 0) return fail(FT_EINVAL, "iterations must be >= 0");
   DeviceGuard g(ctx->device);
   const int64_t n = (int64_t)w * h;
-  FT_TRY(ctx->ensure_scratch((size_t)4 * n * 8));
+  FT_TRY(ctx->ensure_scratch((size_t)5 * n * 8));
   return launch_structure_texture(in, w, h, 0, weight, blend, iterations, out, 0,
                                   (double *)ctx->scratch, 0, 1, ctx->stream);
 }
@@ -299,7 +299,7 @@ int ft_rof_denoise(ft_ctx *ctx, const double *in, int w, int h, double weight, i
   if (iterations < 0) return fail(FT_EINVAL, "iterations must be >= 0");
   DeviceGuard g(ctx->device);
   const int64_t n = (int64_t)w * h;
-  FT_TRY(ctx->ensure_scratch((size_t)4 * n * 8));
+  FT_TRY(ctx->ensure_scratch((size_t)5 * n * 8));
   return launch_structure_texture(in, w, h, 0, weight, 0.0, iterations, out, 0,
                                   (double *)ctx->scratch, 0, 1, ctx->stream, 1, step);
 }
@@ -758,7 +758,7 @@ struct ft_tracker {
       return FT_OK;
     }
     FT_TRY(launch_structure_texture(img, PW, PH, P, cfg.rof_weight, cfg.rof_blend,
-                                    cfg.rof_iterations, d_st, P, d_rofws, 4 * P, S, s, 0, 0.25));
+                                    cfg.rof_iterations, d_st, P, d_rofws, 5 * P, S, s, 0, 0.25));
     phase_mark("structure_texture");
     // (2) flow pyramid of the current ST frame (x255, optflow.py:242-243)
     FT_TRY(build_flow_pyramid(d_st, P, geo, d_fchain, pyr_cur, geo.total, S, s));
@@ -803,7 +803,7 @@ struct ft_tracker {
     }
     phase_mark("ingest+pyramid");
     FT_TRY(launch_structure_texture(img, PW, PH, P, cfg.rof_weight, cfg.rof_blend,
-                                    cfg.rof_iterations, d_st, P, d_rofws, 4 * P, S, s, 0, 0.25));
+                                    cfg.rof_iterations, d_st, P, d_rofws, 5 * P, S, s, 0, 0.25));
     phase_mark("structure_texture");
     FT_TRY(build_flow_pyramid(d_st, P, geo, d_fchain, pyr, geo.total, S, s));
     FT_TRY(launch_keep_prev(pyr, pyr_keep, geo.total, in + 1, S, s));
@@ -1000,7 +1000,7 @@ int ft_tracker_create(ft_ctx *ctx, const ft_tracker_config *cfg, ft_tracker **ou
     FT_TRY(t->alloc(&t->d_kbox, (size_t)S * cfg->max_tracks * 4));
   } else if (cfg->motion == FT_MOTION_TVL1) {
     FT_TRY(t->alloc(&t->d_st, (size_t)S * P));
-    FT_TRY(t->alloc(&t->d_rofws, (size_t)S * 4 * P));
+    FT_TRY(t->alloc(&t->d_rofws, (size_t)S * 5 * P));  // p ping-pong + img/weight
     FT_TRY(t->alloc(&t->d_pyr_prev, (size_t)S * t->geo.total));
     FT_TRY(t->alloc(&t->d_pyr_cur, (size_t)S * t->geo.total));
     FT_TRY(t->alloc(&t->d_fchain, (size_t)S * t->geo.total));

@@ -176,7 +176,8 @@ template <bool P2, bool FIX, int kRBY, int NXC, bool IN>
 __device__ __forceinline__ void rof_tile_body(
     const double *__restrict__ img, int w, int h, int64_t is, const double *__restrict__ px_in,
     const double *__restrict__ py_in, double *__restrict__ px_out, double *__restrict__ py_out,
-    int64_t ps, double weight, double step, int halo, int iters, int first, int cone_on) {
+    int64_t ps, double weight, double step, int halo, int iters, int first, int cone_on,
+    const double *__restrict__ iw_in, double *__restrict__ iw_out) {
   using G = RofGeom<kRBY, NXC>;
   constexpr int kRTH = G::TH, kRPL = G::PL, TW = G::TW, SP = G::SP, NQ = kRPY * NXC;
   extern __shared__ double rof_sm[];
@@ -204,7 +205,9 @@ __device__ __forceinline__ void rof_tile_body(
     const bool in = IN || (gc >= 0 && gc < w && gr >= 0 && gr < h);
     const int64_t o = (int64_t)gr * w + gc;
     const int id0 = (ty + kRBY * (q / NXC) + 1) * SP + tx + 32 * (q % NXC) + 1;
-    ROF_IW(q, id0) = in ? img[o] / weight : 0.0;  // img / weight (imaging.py:121)
+    // img / weight (imaging.py:121): divided by the first launch of the
+    // structure-texture pass, which stores it; later launches read it back
+    ROF_IW(q, id0) = in ? (iw_in ? iw_in[po + o] : img[o] / weight) : 0.0;
     px[q] = (in && !first) ? px_in[po + o] : 0.0;
     py[q] = (in && !first) ? py_in[po + o] : 0.0;
     fR[q] = IN || gc < w - 1;
@@ -265,6 +268,7 @@ __device__ __forceinline__ void rof_tile_body(
     const int64_t o = po + (int64_t)gr * w + gc;
     px_out[o] = px[q];
     py_out[o] = py[q];
+    if (iw_out) iw_out[o] = ROF_IW(q, (lr + 1) * SP + lc + 1);
   }
 #undef ROF_IW
 }
@@ -274,16 +278,19 @@ __global__ void __launch_bounds__(32 * kRBY, kRBY == 16 ? 2 : 1)
     k_rof_tile(const double *__restrict__ img, int w, int h, int64_t is,
                const double *__restrict__ px_in, const double *__restrict__ py_in,
                double *__restrict__ px_out, double *__restrict__ py_out, int64_t ps,
-               double weight, double step, int halo, int iters, int first, int cone_on) {
+               double weight, double step, int halo, int iters, int first, int cone_on,
+               const double *__restrict__ iw_in, double *__restrict__ iw_out) {
   using G = RofGeom<kRBY, NXC>;
   const int hh = FIX ? 4 : halo;
   const int ox = blockIdx.x * (G::TW - 2 * hh) - hh, oy = blockIdx.y * (G::TH - 2 * hh) - hh;
   if (ox >= 1 && ox + G::TW <= w - 1 && oy >= 1 && oy + G::TH <= h - 1)
     rof_tile_body<P2, FIX, kRBY, NXC, true>(img, w, h, is, px_in, py_in, px_out, py_out, ps,
-                                            weight, step, halo, iters, first, cone_on);
+                                            weight, step, halo, iters, first, cone_on, iw_in,
+                                            iw_out);
   else
     rof_tile_body<P2, FIX, kRBY, NXC, false>(img, w, h, is, px_in, py_in, px_out, py_out, ps,
-                                             weight, step, halo, iters, first, cone_on);
+                                             weight, step, halo, iters, first, cone_on, iw_in,
+                                             iw_out);
 }
 
 int grid1d(int64_t n, int bs) {
@@ -356,7 +363,7 @@ int launch_scale_copy(const double *src, int64_t n, int64_t ss, double *dst, int
 int launch_structure_texture(const double *img, int w, int h, int64_t is, double weight,
                              double blend, int iterations, double *out, int64_t os, double *ws,
                              int64_t wss, int nb, cudaStream_t s, int mode, double step) {
-  // ws per image: [px0, py0, px1, py1] planes of w*h
+  // ws per image: [px0, py0, px1, py1, img/weight] planes of w*h
   const int64_t n = (int64_t)w * h;
   for (int b = 0; b < nb; ++b) FT_CUDA_TRY(cudaMemsetAsync(ws + b * wss, 0, 2 * n * 8, s));
   double *p[2][2] = {{ws, ws + n}, {ws + 2 * n, ws + 3 * n}};
@@ -380,9 +387,11 @@ int launch_structure_texture(const double *img, int w, int h, int64_t is, double
                    : (fix ? k_rof_tile<false, true, 16, 2> : k_rof_tile<false, false, 16, 2>);
     FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)G::smem));
+    double *const iw = ws + 4 * n;
     kern<<<g, dim3(32, 16), G::smem, s>>>(img, w, h, is, p[cur][0], p[cur][1], p[1 - cur][0],
                                           p[1 - cur][1], wss, weight, step, halo, k, done == 0,
-                                          1);
+                                          1, done == 0 ? nullptr : iw,
+                                          done == 0 && done + k < iterations ? iw : nullptr);
     count_launch();
     cur = 1 - cur;
     done += k;

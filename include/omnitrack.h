@@ -219,7 +219,9 @@ int ft_tracker_input_buffers(ft_tracker *trk, uint8_t **h_luma, ft_det **h_dets,
  * frame t+1 into slot (t+1)&1 (ft_tracker_slot_buffers, or pass host
  * pointers) and submit it while frame t is still running; wait returns a
  * slot's records.  Submissions execute in order, so results are identical to
- * the synchronous call.  NULL luma/dets/n_dets = already staged in the slot. */
+ * the synchronous call; a submission's H2D copy runs on the tracker's copy
+ * stream while the previous step computes.  NULL luma/dets/n_dets = already
+ * staged in the slot. */
 int ft_tracker_slot_buffers(ft_tracker *trk, int slot, uint8_t **h_luma, ft_det **h_dets,
                             int32_t **h_n_dets);
 int ft_tracker_submit(ft_tracker *trk, int slot, int frame_index, const uint8_t *h_luma,
@@ -272,9 +274,11 @@ int ft_tracker_launches(ft_tracker *trk, int64_t *count);
 /* Per-phase device times of a step (FrameResult carries
  * per-phase timing in ms).  slot 0/1: the step last submitted in that slot
  * (waits for it); slot -1: the most recent step.  Fills up to `max` phases
- * in execution order: ms[i] and names[i] (static strings: "h2d",
- * "ingest+pyramid", "structure_texture", "flow pyramid", "flow level k",
- * "predict+match+update", "d2h", ...); *n = phases written. */
+ * in execution order: ms[i] and names[i] (static strings: "h2d" (prefetch
+ * trackers; the others copy a submission's inputs on a copy stream while the
+ * previous step runs), "ingest+pyramid", "structure_texture", "flow
+ * pyramid", "flow level k", "predict+match+update", "d2h", ...); *n = phases
+ * written. */
 int ft_tracker_phase_times(ft_tracker *trk, int slot, double *ms, const char **names, int max,
                            int *n);
 /* Reset all streams (drop tracks and cached previous frames).  Submitted

@@ -622,6 +622,16 @@ struct ft_tracker {
   // records of frame k-1 come back with step k (one-frame lag), a flush step
   // tracks the last frame.  Three rotating flow pyramids (frame k being
   // built, k-1 and k-2 being read) and per-parity device inputs.
+  // host-I/O submissions (non-prefetch): a slot's inputs go H2D on the copy
+  // stream `cstream` into the slot's own device buffers while the step in
+  // flight computes; the step graph waits on ev_h2d[slot], and the next H2D
+  // into that slot waits on ev_used[slot] (the end of the step that read it)
+  cudaStream_t cstream = nullptr;
+  uint8_t *d_luma_s[2] = {};
+  ft_det *d_dets_s[2] = {};
+  int32_t *d_in_s[2] = {};
+  cudaEvent_t ev_h2d[2] = {}, ev_used[2] = {};
+  bool used_rec[2] = {};
   int prefetch = 0;
   cudaStream_t stream2 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -694,14 +704,17 @@ struct ft_tracker {
   }
 
   // enqueue one step on `s` reading luma/dets/in from the given device ptrs
+  // io: 1 = copy the staged inputs H2D inside the graph, 2 = copy the track
+  // tables D2H inside the graph
   int enqueue(cudaStream_t s, bool has_prev, const uint8_t *luma, const ft_det *dets,
-              const int32_t *in, bool host_io) {
+              const int32_t *in, int io) {
+    const bool host_in = io & 1, host_out = io & 2;
     // pyramid ping-pong: this step builds into `pyr_cur`, the previous step's
     // pyramid is `pyr_prev` (pyr_par flips after every step; no copy)
     double *const pyr_cur = pyr_par ? d_pyr_prev : d_pyr_cur;
     double *const pyr_prev = pyr_par ? d_pyr_cur : d_pyr_prev;
     phase_mark("start");
-    if (host_io) {
+    if (host_in) {
       FT_CUDA_TRY(cudaMemcpyAsync(d_luma, h_luma, (size_t)S * W * H, cudaMemcpyHostToDevice, s));
       FT_CUDA_TRY(cudaMemcpyAsync(d_dets, h_dets, (size_t)S * cfg.max_dets * sizeof(ft_det),
                                   cudaMemcpyHostToDevice, s));
@@ -748,7 +761,7 @@ struct ft_tracker {
       FT_TRY(launch_tracker_track(T, nullptr, nullptr, P, PW, PH, L, dets, in + 1, in + 1 + S,
                                   has_prev, d_out, d_nout, s, kbox));
       phase_mark("predict+match+update");
-      if (host_io) {
+      if (host_out) {
         FT_CUDA_TRY(cudaMemcpyAsync(h_out, d_out,
                                     (size_t)S * 2 * cfg.max_tracks * sizeof(ft_track),
                                     cudaMemcpyDeviceToHost, s));
@@ -775,7 +788,7 @@ struct ft_tracker {
     FT_TRY(launch_tracker_track(T, d_dx, d_dy, P, PW, PH, L, dets, in + 1, in + 1 + S, has_prev,
                                 d_out, d_nout, s));
     phase_mark("predict+match+update");
-    if (host_io) {
+    if (host_out) {
       FT_CUDA_TRY(cudaMemcpyAsync(h_out, d_out, (size_t)S * 2 * cfg.max_tracks * sizeof(ft_track),
                                   cudaMemcpyDeviceToHost, s));
       FT_CUDA_TRY(cudaMemcpyAsync(h_nout, d_nout, (size_t)2 * S * 4, cudaMemcpyDeviceToHost, s));
@@ -918,13 +931,14 @@ struct ft_tracker {
     return FT_OK;
   }
 
-  int run(bool has_prev, const uint8_t *luma, const ft_det *dets, const int32_t *in,
-          bool host_io) {
-    // host-I/O graphs bake the staging slot's pinned pointers into their
-    // copy nodes: key them by those pointers (one graph per slot)
-    GraphKey key{(has_prev ? 1 : 0) | (pyr_par << 1), host_io ? (const void *)h_luma : luma,
-                 host_io ? (const void *)h_dets : dets, host_io ? (const void *)h_in : in};
-    FT_TRY(launch_graph(key, [&] { return enqueue(stream, has_prev, luma, dets, in, host_io); }));
+  int run(bool has_prev, const uint8_t *luma, const ft_det *dets, const int32_t *in, int io) {
+    // graphs with copy nodes bake the staging slot's pinned pointers in: key
+    // them by those pointers (one graph per slot; io = 2 graphs read the
+    // slot's own device inputs, so their input pointers identify the slot)
+    GraphKey key{(has_prev ? 1 : 0) | (pyr_par << 1) | (io << 2),
+                 (io & 1) ? (const void *)h_luma : luma, (io & 1) ? (const void *)h_dets : dets,
+                 (io & 1) ? (const void *)h_in : in};
+    FT_TRY(launch_graph(key, [&] { return enqueue(stream, has_prev, luma, dets, in, io); }));
     pyr_par ^= 1;
     return FT_OK;
   }
@@ -1065,6 +1079,16 @@ int ft_tracker_create(ft_ctx *ctx, const ft_tracker_config *cfg, ft_tracker **ou
     FT_CUDA_TRY(cudaMallocHost(&sl.nout, (size_t)2 * S * 4));
     FT_CUDA_TRY(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
   }
+  if (!t->prefetch) {
+    FT_CUDA_TRY(cudaStreamCreateWithFlags(&t->cstream, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+      FT_TRY(t->alloc(&t->d_luma_s[k], (size_t)S * t->W * t->H));
+      FT_TRY(t->alloc(&t->d_dets_s[k], (size_t)S * D));
+      FT_TRY(t->alloc(&t->d_in_s[k], (size_t)2 * S + 1));
+      FT_CUDA_TRY(cudaEventCreateWithFlags(&t->ev_h2d[k], cudaEventDisableTiming));
+      FT_CUDA_TRY(cudaEventCreateWithFlags(&t->ev_used[k], cudaEventDisableTiming));
+    }
+  }
   t->use_slot(0);
   *out = t.release();
   return ft_tracker_reset(*out);
@@ -1121,6 +1145,14 @@ int ft_tracker_destroy(ft_tracker *t) {
   if (t->ev_fork) cudaEventDestroy(t->ev_fork);
   if (t->ev_join) cudaEventDestroy(t->ev_join);
   if (t->stream2) cudaStreamDestroy(t->stream2);
+  if (t->cstream) {
+    cudaStreamSynchronize(t->cstream);
+    cudaStreamDestroy(t->cstream);
+  }
+  for (int k = 0; k < 2; ++k) {
+    if (t->ev_h2d[k]) cudaEventDestroy(t->ev_h2d[k]);
+    if (t->ev_used[k]) cudaEventDestroy(t->ev_used[k]);
+  }
   if (t->ev_in) cudaEventDestroy(t->ev_in);
   if (t->ev_out) cudaEventDestroy(t->ev_out);
   if (t->stream) cudaStreamDestroy(t->stream);
@@ -1154,7 +1186,21 @@ static int submit_slot(ft_tracker *t, int slot, bool new_frame = true) {
     FT_TRY(t->run_prefetch(new_frame, &rec));
     sl.records = rec;
   } else {
-    FT_TRY(t->run(t->frames_seen > 0, nullptr, nullptr, nullptr, true));
+    // H2D on the copy stream into the slot's device inputs (overlaps the
+    // step in flight), the step graph after it
+    const size_t nl = (size_t)t->S * t->W * t->H;
+    if (t->used_rec[slot]) FT_CUDA_TRY(cudaStreamWaitEvent(t->cstream, t->ev_used[slot], 0));
+    FT_CUDA_TRY(cudaMemcpyAsync(t->d_luma_s[slot], sl.luma, nl, cudaMemcpyHostToDevice, t->cstream));
+    FT_CUDA_TRY(cudaMemcpyAsync(t->d_dets_s[slot], sl.dets,
+                                (size_t)t->S * t->cfg.max_dets * sizeof(ft_det),
+                                cudaMemcpyHostToDevice, t->cstream));
+    FT_CUDA_TRY(cudaMemcpyAsync(t->d_in_s[slot], sl.in, (size_t)(2 * t->S + 1) * 4,
+                                cudaMemcpyHostToDevice, t->cstream));
+    FT_CUDA_TRY(cudaEventRecord(t->ev_h2d[slot], t->cstream));
+    FT_CUDA_TRY(cudaStreamWaitEvent(t->stream, t->ev_h2d[slot], 0));
+    FT_TRY(t->run(t->frames_seen > 0, t->d_luma_s[slot], t->d_dets_s[slot], t->d_in_s[slot], 2));
+    FT_CUDA_TRY(cudaEventRecord(t->ev_used[slot], t->stream));
+    t->used_rec[slot] = true;
     sl.records = true;
   }
   sl.graph = t->last_graph;
@@ -1293,7 +1339,7 @@ int ft_tracker_step_device(ft_tracker *t, const uint8_t *d_luma, int frame, cons
                               cudaMemcpyDeviceToDevice, s));
   FT_CUDA_TRY(cudaMemcpyAsync(t->d_dets, d_dets, (size_t)t->S * t->cfg.max_dets * sizeof(ft_det),
                               cudaMemcpyDeviceToDevice, s));
-  FT_TRY(t->run(t->frames_seen > 0, t->d_luma, t->d_dets, t->d_in, false));
+  FT_TRY(t->run(t->frames_seen > 0, t->d_luma, t->d_dets, t->d_in, 0));
   t->frames_seen++;
   return t->join_out();
 }

@@ -336,8 +336,10 @@ class Tracker:
     def phase_ms(self, slot: int = -1) -> dict:
         """Per-phase device times (ms) of a step: slot 0/1 =
         the step last submitted in that slot, -1 = the most recent step.
-        Keys in execution order ("h2d", "ingest+pyramid", "structure_texture",
-        "flow pyramid", "flow level k" ..., "predict+match+update", "d2h")."""
+        Keys in execution order ("ingest+pyramid", "structure_texture",
+        "flow pyramid", "flow level k" ..., "predict+match+update", "d2h"; a
+        prefetch tracker's step starts with "h2d" -- the other trackers copy
+        their inputs on a copy stream, overlapped with the previous step)."""
         n = C.c_int()
         ms = (C.c_double * 32)()
         names = (C.c_char_p * 32)()

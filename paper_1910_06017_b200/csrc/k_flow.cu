@@ -161,15 +161,32 @@ __global__ void k_warp_setup(const double *__restrict__ i0, const double *__rest
 }
 
 // 3x3 median with replicated border (imageops.py:78-84): exact 5th order
-// statistic of 9 via a min/max selection network.
+// statistic of 9 via a min/max selection network.  One comparison per
+// compare-swap (the fields are finite: MotionField / compute_flow reject
+// NaN, optflow.py:85-86); a tie between -0.0 and +0.0 may return either
+// zero, as numpy's introselect may (np.median's partition is not
+// order-stable).
 __device__ __forceinline__ void cswap(double &a, double &b) {
-  const double lo = fmin(a, b), hi = fmax(a, b);
+  const bool sw = b < a;
+  const double lo = sw ? b : a, hi = sw ? a : b;
   a = lo;
   b = hi;
 }
 
 __device__ __forceinline__ double med3(double a, double b, double c) {
-  return fmax(fmin(a, b), fmin(fmax(a, b), c));
+  cswap(a, b);                 // a <= b
+  const double m = c < b ? c : b;  // min(max(a, b), c)
+  return m < a ? a : m;        // max(min(a, b), min(max(a, b), c))
+}
+
+__device__ __forceinline__ double max3(double a, double b, double c) {
+  const double m = b < a ? a : b;
+  return c < m ? m : c;
+}
+
+__device__ __forceinline__ double min3(double a, double b, double c) {
+  const double m = b < a ? b : a;
+  return c < m ? c : m;
 }
 
 // Two horizontally adjacent outputs per thread: the four 3-sample columns
@@ -205,10 +222,10 @@ __global__ void k_median(const double2 *__restrict__ in, double2 *__restrict__ o
   double m[2][2];
 #pragma unroll
   for (int f = 0; f < 2; ++f) {
-    m[f][0] = med3(fmax(fmax(lo[f][0], lo[f][1]), lo[f][2]), med3(md[f][0], md[f][1], md[f][2]),
-                   fmin(fmin(hi[f][0], hi[f][1]), hi[f][2]));
-    m[f][1] = med3(fmax(fmax(lo[f][1], lo[f][2]), lo[f][3]), med3(md[f][1], md[f][2], md[f][3]),
-                   fmin(fmin(hi[f][1], hi[f][2]), hi[f][3]));
+    m[f][0] = med3(max3(lo[f][0], lo[f][1], lo[f][2]), med3(md[f][0], md[f][1], md[f][2]),
+                   min3(hi[f][0], hi[f][1], hi[f][2]));
+    m[f][1] = med3(max3(lo[f][1], lo[f][2], lo[f][3]), med3(md[f][1], md[f][2], md[f][3]),
+                   min3(hi[f][1], hi[f][2], hi[f][3]));
   }
   double2 *o = out + so + (int64_t)r * w + c;
   o[0] = make_double2(m[0][0], m[1][0]);

@@ -558,6 +558,10 @@ __device__ __forceinline__ void pd_halfsteps_cq(const PDArgs &a, double *sm, int
     // middle launch (P D)x4 of a 32-row tile with halo 4: the cone rows of
     // halfstep_schedule in closed form -- P_i: [1+i, 32-i), D_i: [1+i, 31-i)
     static_assert(!MID || TH == 32, "closed-form cone is for 32-row tiles");
+    // fully unrolled: the pixel state alternates between register sets
+    // instead of being moved back every iteration, and no spills remain
+    // (+0.4 %; unrolling by 2 was slower)
+#pragma unroll
     for (int i = 0; i < 4; ++i) {
       half(false, 1 + i, TH - i);
       half(true, 1 + i, TH - 1 - i);

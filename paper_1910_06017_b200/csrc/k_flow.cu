@@ -424,7 +424,10 @@ __device__ __forceinline__ double madx(double a, double b, double c) {
 // of every warp running the hypot + division code for its own ~4 pairs with
 // most lanes idle).  Primal half-step: reads its p from shared memory.
 // Same arithmetic in the same order as the reference iteration.
-template <int TW, int BY, int PY, bool P2, bool IN, bool MID>
+// launch schedules with compile-time half-step order (k_pd_tile MODE)
+enum : int { kSchedGeneric = 0, kSchedMid = 1, kSchedFirst = 2, kSchedLast = 3 };
+
+template <int TW, int BY, int PY, bool P2, bool IN, int MODE>
 __device__ __forceinline__ void pd_halfsteps_cq(const PDArgs &a, double *sm, int base, int tx,
                                                 int ty, const unsigned *fl, double *u1,
                                                 double *u2, const double *gx, const double *gy,
@@ -554,10 +557,10 @@ __device__ __forceinline__ void pd_halfsteps_cq(const PDArgs &a, double *sm, int
     }
     __syncthreads();
   };
-  if (MID) {
+  if (MODE == kSchedMid) {
     // middle launch (P D)x4 of a 32-row tile with halo 4: the cone rows of
     // halfstep_schedule in closed form -- P_i: [1+i, 32-i), D_i: [1+i, 31-i)
-    static_assert(!MID || TH == 32, "closed-form cone is for 32-row tiles");
+    static_assert(MODE != kSchedMid || TH == 32, "closed-form cone is for 32-row tiles");
     // fully unrolled: the pixel state alternates between register sets
     // instead of being moved back every iteration, and no spills remain
     // (+0.4 %; unrolling by 2 was slower)
@@ -566,6 +569,14 @@ __device__ __forceinline__ void pd_halfsteps_cq(const PDArgs &a, double *sm, int
       half(false, 1 + i, TH - i);
       half(true, 1 + i, TH - 1 - i);
     }
+  } else if (MODE == kSchedFirst) {
+    // a warp's first launch: D P D P D P D, cone rows from the schedule
+#pragma unroll
+    for (int j = 0; j < 7; ++j) half((j & 1) == 0, a.rows_lo[j], a.rows_hi[j]);
+  } else if (MODE == kSchedLast) {
+    // a warp's last launch: P D P D P
+#pragma unroll
+    for (int j = 0; j < 5; ++j) half((j & 1) == 1, a.rows_lo[j], a.rows_hi[j]);
   } else {
     for (int j = 0; j < a.nhalf; ++j) {
       const bool dual = ((j & 1) == 0) == (a.first != 0);
@@ -580,7 +591,7 @@ __device__ __forceinline__ void pd_halfsteps_cq(const PDArgs &a, double *sm, int
 // PX / PY with TMA box stores from a shared staging area.  Out-of-image
 // elements are zero-filled on load (the reference's zeros outside the
 // image never reach an interior pixel) and clipped on store.
-template <int TW, int BY, int PY, int MINB, bool MID = false>
+template <int TW, int BY, int PY, int MINB, int MODE = kSchedGeneric>
 __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const __grid_constant__ PDArgs a) {
   using G = PDGeom<TW, BY, PY>;
   constexpr int NX = G::NX, TH = G::TH, NP = G::NP, SP = G::SP, SR = G::SR, PL = G::PLANE;
@@ -671,7 +682,7 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const __grid_constant
   const bool interior = ox >= 1 && oy >= 1 && ox + TW <= W - 1 && oy + TH <= H - 1;
   {
 #define FT_PD_CALL(P2_, IN_)                                                                 \
-  pd_halfsteps_cq<TW, BY, PY, P2_, IN_, MID>(a, sm, base, tx, ty, fl, u1, u2, gx, gy, \
+  pd_halfsteps_cq<TW, BY, PY, P2_, IN_, MODE>(a, sm, base, tx, ty, fl, u1, u2, gx, gy, \
                                              stage + TW * TH, thr_, tl, qidx, ctr)
     if (a.pow2) {
       if (interior) FT_PD_CALL(true, true); else FT_PD_CALL(true, false);
@@ -715,15 +726,21 @@ __global__ void __launch_bounds__(32 * BY, MINB) k_pd_tile(const __grid_constant
 struct PDConfig {
   int tw, th, by;
   void (*fn)(PDArgs);
-  void (*fn_mid)(PDArgs);  // k_pd_tile<..., MID>: middle (P D)x4 launches, halo 4
+  void (*fn_mid)(PDArgs);    // k_pd_tile<..., kSchedMid>: middle (P D)x4 launches, halo 4
+  void (*fn_first)(PDArgs);  // kSchedFirst: a warp's first launch (7 half-steps)
+  void (*fn_last)(PDArgs);   // kSchedLast: a warp's last launch (5 half-steps)
   size_t smem;             // exchange planes, TMA staging, projection queue, mbarrier
 };
 
 template <int TW, int BY, int PY, int MINB>
 PDConfig make_cfg() {
   using G = PDGeom<TW, BY, PY>;
+  constexpr bool t32 = G::TH == 32 && TW == 32 && BY == 16;  // the tiled configuration
   return PDConfig{TW, G::TH, BY, &k_pd_tile<TW, BY, PY, MINB>,
-                  G::TH == 32 ? &k_pd_tile<TW, BY, PY, MINB, G::TH == 32> : nullptr, G::smem};
+                  G::TH == 32 ? &k_pd_tile<TW, BY, PY, MINB, kSchedMid> : nullptr,
+                  t32 ? &k_pd_tile<TW, BY, PY, MINB, t32 ? kSchedFirst : kSchedGeneric> : nullptr,
+                  t32 ? &k_pd_tile<TW, BY, PY, MINB, t32 ? kSchedLast : kSchedGeneric> : nullptr,
+                  G::smem};
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no
@@ -781,7 +798,9 @@ int pd_launch(const PDConfig &c, PDArgs &a, const StatePtrs &in, const StatePtrs
   FT_TRY(plane_map(&a.out_py, out.py, a.w, a.h, nb, cap, iw, ih));
   const bool mid = c.fn_mid && !a.first && !a.last && a.nhalf == 8 && a.halo == 4 && a.cone_rows &&
                    c.th == 32;
-  void (*fn)(PDArgs) = mid ? c.fn_mid : c.fn;
+  const bool first7 = c.fn_first && a.first && !a.last && a.nhalf == 7 && a.cone_rows;
+  const bool last5 = c.fn_last && !a.first && a.last && a.nhalf == 5 && a.cone_rows;
+  void (*fn)(PDArgs) = mid ? c.fn_mid : first7 ? c.fn_first : last5 ? c.fn_last : c.fn;
   FT_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem));
   int dev = 0, sms = kSMs, per_sm = 0;
   FT_CUDA_TRY(cudaGetDevice(&dev));

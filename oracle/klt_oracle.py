@@ -114,6 +114,7 @@ def lk_track(src_pyr, src_grad, dst_pyr, px: float, py: float):
         if not det >= MIN_DET:
             ok = False
             break
+        idet = 1.0 / det  # once per level; the steps multiply by it
         vx, vy = 0.0, 0.0
         for _ in range(ITERS):
             qx, qy = cx + gx_ + vx, cy + gy_ + vy
@@ -121,8 +122,8 @@ def lk_track(src_pyr, src_grad, dst_pyr, px: float, py: float):
             dI = [iv - jj for iv, jj in zip(ivs, jv)]
             bx = lane_sum([d * a for d, a in zip(dI, ixs)])
             by = lane_sum([d * b for d, b in zip(dI, iys)])
-            ex = (gyy * bx - gxy * by) / det
-            ey = (gxx * by - gxy * bx) / det
+            ex = (gyy * bx - gxy * by) * idet
+            ey = (gxx * by - gxy * bx) * idet
             vx = vx + ex
             vy = vy + ey
             if ex * ex + ey * ey < EPS_STEP * EPS_STEP:

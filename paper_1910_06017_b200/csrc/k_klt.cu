@@ -123,6 +123,7 @@ __device__ bool lk_point(const KltPyr &A, const KltPyr &B, int img, double px, d
       ok = false;
       break;
     }
+    const double idet = 1.0 / det;  // once per level (klt_oracle.lk_track)
     double vx = 0.0, vy = 0.0;
     for (int it = 0; it < kKltIters; ++it) {
       const double qx_ = cx + ga + vx, qy_ = cy + gb + vy;
@@ -140,8 +141,8 @@ __device__ bool lk_point(const KltPyr &A, const KltPyr &B, int img, double px, d
       }
       double bx, by;
       warp_sum2(bxp, byp, bx, by);
-      const double ex = (gyy * bx - gxy * by) / det;
-      const double ey = (gxx * by - gxy * bx) / det;
+      const double ex = (gyy * bx - gxy * by) * idet;
+      const double ey = (gxx * by - gxy * bx) * idet;
       vx = vx + ex;
       vy = vy + ey;
       if (ex * ex + ey * ey < kKltEps * kKltEps) break;

@@ -22,8 +22,9 @@ Algorithm (per box, frames at the tracker's processing level L):
    same binomial pyramid as the flow path, window (2R+1)^2 sampled with one
    shared bilinear fraction per window (see `window`), central gradients of
    the source level, up to ITERS Gauss-Newton steps per level
-   (stop when |eta| < EPS_STEP), a point is lost when the structure tensor
-   determinant is < MIN_DET or it leaves the level;
+   (stop when |eta| < EPS_STEP; the 2x2 solve multiplies by 1/det, divided
+   once per level), a point is lost when the structure tensor determinant is
+   < MIN_DET or it leaves the level;
 3. the same tracking back curr -> prev; fb = |p_back - p|;
 4. keep valid points with fb <= lower-median(fb of valid points);
 5. shift = lower-median of kept dx, dy; scale = lower-median of

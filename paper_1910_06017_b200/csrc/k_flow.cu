@@ -449,7 +449,9 @@ __device__ __forceinline__ void pd_halfsteps_cq(const PDArgs &a, double *sm, int
   // both spill at the 64-register cap (+1.4 % vs 0.6 % for px alone, -0.1 %
   // for three of the four double2)
   constexpr int KEEPP = (MODE == kSchedMid) ? 1 : 0;
-  double2 kpx[NP], kpy[NP];
+  double2 kpx[NP], kpy[NP];  // set by every MID primal step before its dual reads them
+#pragma unroll
+  for (int q = 0; q < NP; ++q) kpx[q] = kpy[q] = make_double2(0.0, 0.0);
   auto half = [&](const bool dual, const int lo, const int hi) {
     bool row_on[NP];
     bool all = true;

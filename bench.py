@@ -217,6 +217,46 @@ def _cpu_frame_job(args):
     return time.perf_counter() - t0
 
 
+def _cv2_frame_job(g: int) -> float:
+    """The KLT backend's practical CPU comparison (informative, not the
+    oracle: OpenCV's fp32 pyramidal LK is not bit-identical): frame 1 of
+    stream g -- the frame-0 detection boxes' 10x10 point grids tracked
+    forward and back with cv2.calcOpticalFlowPyrLK (9x9 window, 3 levels,
+    10 iterations, eps 0.01 px) on one core."""
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    import cv2
+    cv2.setNumThreads(1)
+    frames, dets = gen_stream(g, 2)
+    pts = []
+    for d in dets[0] or []:
+        x, y, w, h = d.box
+        for j in range(10):
+            for i in range(10):
+                pts.append((x + (i + 0.5) * w / 10, y + (j + 0.5) * h / 10))
+    p0 = np.asarray(pts, dtype=np.float32).reshape(-1, 1, 2)
+    a, b = np.ascontiguousarray(frames[0]), np.ascontiguousarray(frames[1])
+    crit = (cv2.TERM_CRITERIA_COUNT | cv2.TERM_CRITERIA_EPS, 10, 0.01)
+    t0 = time.perf_counter()
+    p1, _, _ = cv2.calcOpticalFlowPyrLK(a, b, p0, None, winSize=(9, 9), maxLevel=2, criteria=crit)
+    cv2.calcOpticalFlowPyrLK(b, a, p1, None, winSize=(9, 9), maxLevel=2, criteria=crit)
+    return time.perf_counter() - t0
+
+
+def cpu_opencv_measure() -> dict:
+    cores = host_cores()
+    ctx = mp.get_context("spawn")
+    t0 = time.perf_counter()
+    with ctx.Pool(cores) as pool:
+        per = pool.map(_cv2_frame_job, list(range(cores)))
+    wall = time.perf_counter() - t0
+    fps = cores / float(np.mean(per))
+    return {"value": round(fps, 3), "unit": "frames/s", "cores": cores,
+            "sample": f"{cores} processes, frame 1 of streams 0..{cores - 1}: "
+                      f"cv2.calcOpticalFlowPyrLK forward + backward on the {N_OBJ} boxes' 10x10 "
+                      "grids (fp32, not bit-identical to the KLT oracle; informative)",
+            "wall_s": round(wall, 1)}
+
+
 def cpu_run(n_procs: int, jobs: int, flow: str, config: str, motion: str):
     for var in ("OMP_NUM_THREADS", "MKL_NUM_THREADS", "OPENBLAS_NUM_THREADS"):
         os.environ[var] = "1"  # one core per process (children inherit)
@@ -460,6 +500,8 @@ def run_ours(args, ws, rank, local):
                                    "0 on the host (torch.distributed gather_object)"}}
         if latency:
             line["latency"] = latency
+        if cpu is not None and args.motion == "klt":
+            line["cpu_opencv"] = cpu_opencv_measure()
         if cpu is None and ws > 1:
             line["cpu_baseline_note"] = "timed at N=1 only (same host, same workload)"
         print(json.dumps(line), flush=True)

@@ -7,7 +7,7 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv 
 timeout 1500 python -m pytest tests -m gpu -q > $O/r02_pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 $O/r02_pytest_gpu.log
 timeout 900 python bench.py > $O/r02_bench_default.jsonl 2> $O/r02_bench_default.err; echo "default rc=$?"
 timeout 600 python bench.py --flow light --no-cpu-baseline > $O/r02_bench_light.jsonl 2>&1; echo "light rc=$?"
-timeout 600 python bench.py --motion klt --no-cpu-baseline > $O/r02_bench_klt.jsonl 2>&1; echo "klt rc=$?"
+timeout 900 python bench.py --motion klt > $O/r02_bench_klt.jsonl 2>&1; echo "klt rc=$?"
 timeout 600 python bench.py --config c3 --streams 32 --no-cpu-baseline > $O/r02_bench_c3.jsonl 2>&1; echo "c3 rc=$?"
 timeout 600 python bench.py --config c4 --streams 8 --no-cpu-baseline > $O/r02_bench_c4.jsonl 2>&1; echo "c4 rc=$?"
 timeout 600 python bench.py --streams 1 --steps 20 --no-cpu-baseline > $O/r02_bench_single.jsonl 2>&1; echo "single rc=$?"

@@ -253,8 +253,10 @@ __device__ __forceinline__ void rof_tile_body(
       // exactly like the reference's separate multiply and add
       const double hy = glibc_hypot(gx, gy);
       const double norm = P2 ? fma(step, hy, 1.0) : 1.0 + step * hy;
-      px[q] = div_pos(P2 ? fma(step, gx, px[q]) : px[q] + step * gx, norm);  // norm >= 1
-      py[q] = div_pos(P2 ? fma(step, gy, py[q]) : py[q] + step * gy, norm);
+      // both components by the same norm: one division (div_by_recip)
+      const double y = 1.0 / norm;  // norm >= 1
+      px[q] = div_by_recip(P2 ? fma(step, gx, px[q]) : px[q] + step * gx, norm, y);
+      py[q] = div_by_recip(P2 ? fma(step, gy, py[q]) : py[q] + step * gy, norm, y);
       s_px[id] = px[q];
       s_py[id] = py[q];
     }
